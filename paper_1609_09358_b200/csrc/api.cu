@@ -1,0 +1,177 @@
+// api.cu -- the C-ABI (include/polarcuda.h): validation, then the launchers.
+#include "args.cuh"
+
+using namespace pc;
+
+static int check_code(const pc_code_t *c)
+{
+    if (c == nullptr || c->N < 2 || c->n < 1 || c->n > PC_MAX_LOGN || (1 << c->n) != c->N)
+        return PC_ERR_INVALID;
+    if (c->k < 1 || c->k > c->N || c->m < 0 || c->m != c->k - c->crc_width)
+        return PC_ERR_INVALID;
+    if (c->crc_width != 0 && c->crc_width != 8 && c->crc_width != 16 && c->crc_width != 24)
+        return PC_ERR_INVALID;
+    if (c->frozen_bits == nullptr || c->info_pos == nullptr)
+        return PC_ERR_INVALID;
+    return PC_OK;
+}
+
+extern "C" {
+
+int pc_version(void) { return 1; }
+
+const char *pc_strerror(int code)
+{
+    switch (code) {
+    case PC_OK: return "ok";
+    case PC_ERR_INVALID: return "invalid argument";
+    case PC_ERR_UNSUPPORTED: return "configuration not supported by the compiled kernels";
+    case PC_ERR_CUDA: return "CUDA runtime error";
+    case PC_ERR_NO_DEVICE: return "no sm_100 CUDA device";
+    default: return "unknown error";
+    }
+}
+
+int64_t pc_workspace_bytes(void) { return 256; }
+
+int pc_device_count(void)
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int good = 0;
+    for (int d = 0; d < n; ++d) {
+        int major = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d) == cudaSuccess && major == 10)
+            ++good;
+    }
+    return good;
+}
+
+int pc_bp_decode(const float *llr, int32_t B, const pc_code_t *code, const pc_bp_cfg_t *cfg, uint32_t *u_bits,
+                 uint32_t *payload, float *soft_u, float *soft_x, int32_t *iters, uint8_t *converged,
+                 uint64_t *t_done, void *stream)
+{
+    int rc = check_code(code);
+    if (rc)
+        return rc;
+    if (cfg == nullptr || B < 0 || (B > 0 && (llr == nullptr || iters == nullptr || converged == nullptr)))
+        return PC_ERR_INVALID;
+    if (cfg->i_max < 1 || cfg->g_mode < 0 || cfg->g_mode > 1 || cfg->stop_mode < 0 || cfg->stop_mode > 2 ||
+        !(cfg->llr_max > 0.0f))
+        return PC_ERR_INVALID;
+    if (cfg->stop_mode == 0 && (code->crc_width == 0 || code->crc_cols == nullptr))
+        return PC_ERR_INVALID;
+    BpArgs a;
+    a.llr = llr;
+    a.B = B;
+    a.code = to_device_code(*code);
+    a.i_max = cfg->i_max;
+    a.stop_mode = cfg->stop_mode;
+    a.llr_max = cfg->llr_max;
+    a.u_bits = u_bits;
+    a.payload = payload;
+    a.soft_u = soft_u;
+    a.soft_x = soft_x;
+    a.iters = iters;
+    a.conv = converged;
+    a.t_done = t_done;
+    return launch_bp_decode(a, cfg->g_mode, cfg->threads_per_frame, (cudaStream_t)stream);
+}
+
+int pc_bp_iterate(float *l_msgs, float *r_msgs, int32_t B, const pc_code_t *code, const pc_bp_cfg_t *cfg,
+                  void *stream)
+{
+    int rc = check_code(code);
+    if (rc)
+        return rc;
+    if (cfg == nullptr || B < 0 || (B > 0 && (l_msgs == nullptr || r_msgs == nullptr)) || cfg->g_mode < 0 ||
+        cfg->g_mode > 1 || !(cfg->llr_max > 0.0f))
+        return PC_ERR_INVALID;
+    return launch_bp_iterate(l_msgs, r_msgs, B, code->n, cfg->g_mode, cfg->llr_max, (cudaStream_t)stream);
+}
+
+int pc_compact(const uint8_t *converged, int32_t B, int32_t *queue, int32_t *count, void *workspace, void *stream)
+{
+    (void)workspace;
+    if (B < 0 || count == nullptr || (B > 0 && (converged == nullptr || queue == nullptr)))
+        return PC_ERR_INVALID;
+    return launch_compact(converged, B, queue, count, (cudaStream_t)stream);
+}
+
+int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32_t *count, const pc_code_t *code,
+                  const pc_scl_cfg_t *cfg, uint32_t *u_bits, uint32_t *payload, float *metric, uint8_t *crc_ok,
+                  uint8_t *sel_by_crc, uint64_t *t_done, void *workspace, void *stream)
+{
+    int rc = check_code(code);
+    if (rc)
+        return rc;
+    if (cfg == nullptr || B < 0 || workspace == nullptr || (B > 0 && llr == nullptr))
+        return PC_ERR_INVALID;
+    const int L = cfg->L;
+    if (L < 1 || L > PC_MAX_LIST || (L & (L - 1)) != 0)
+        return PC_ERR_UNSUPPORTED;
+    if (code->crc_width > 0 && code->crc_cols == nullptr)
+        return PC_ERR_INVALID;
+    SclArgs a;
+    a.llr = llr;
+    a.B = B;
+    a.queue = queue;
+    a.count = count;
+    a.code = to_device_code(*code);
+    a.metric_exact = cfg->metric_exact;
+    a.f_exact = cfg->f_exact;
+    a.u_bits = u_bits;
+    a.payload = payload;
+    a.metric = metric;
+    a.crc_ok = crc_ok;
+    a.sel = sel_by_crc;
+    a.t_done = t_done;
+    a.work = reinterpret_cast<int32_t *>(workspace);
+    int nv = cfg->virtual_levels;
+    if (nv < 0)
+        nv = code->n >= 10 ? 2 : 0;
+    scl_prepare(a, nv);
+    return launch_scl(a, L, cfg->warps_per_cta, (cudaStream_t)stream);
+}
+
+int pc_encode(const uint32_t *msg_bits, int32_t B, const pc_code_t *code, uint32_t *x_bits, void *stream)
+{
+    int rc = check_code(code);
+    if (rc)
+        return rc;
+    if (B < 0 || (B > 0 && (msg_bits == nullptr || x_bits == nullptr)) ||
+        (code->crc_width > 0 && code->enc_cols == nullptr))
+        return PC_ERR_INVALID;
+    return launch_encode(to_device_code(*code), msg_bits, B, x_bits, (cudaStream_t)stream);
+}
+
+int pc_gen_frames(uint64_t seed, int32_t point, int64_t frame0, int32_t B, float sigma, const pc_code_t *code,
+                  uint32_t *msg_bits, float *llr, void *stream)
+{
+    int rc = check_code(code);
+    if (rc)
+        return rc;
+    if (B < 0 || (B > 0 && llr == nullptr) || !(sigma >= 0.0f) || (code->crc_width > 0 && code->enc_cols == nullptr))
+        return PC_ERR_INVALID;
+    return launch_gen(to_device_code(*code), seed, point, frame0, B, sigma, msg_bits, llr, (cudaStream_t)stream);
+}
+
+int pc_count_errors(const uint32_t *payload, const uint32_t *msg_bits, int32_t B, int32_t m, int64_t *counters,
+                    void *stream)
+{
+    if (B < 0 || m < 1 || counters == nullptr || (B > 0 && (payload == nullptr || msg_bits == nullptr)))
+        return PC_ERR_INVALID;
+    return launch_count_errors(payload, msg_bits, B, m, counters, (cudaStream_t)stream);
+}
+
+int pc_stamp(uint64_t *t, void *stream)
+{
+    if (t == nullptr)
+        return PC_ERR_INVALID;
+    return launch_stamp(t, (cudaStream_t)stream);
+}
+
+} // extern "C"

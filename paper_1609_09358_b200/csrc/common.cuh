@@ -1,0 +1,66 @@
+// common.cuh -- device helpers shared by the sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "polarcuda.h"
+
+#define PC_LOG2E 1.4426950408889634f
+#define PC_LN2 0.6931471805599453f
+
+namespace pc {
+
+// MUFU (XU pipe) approximations; flush-to-zero keeps them single-instruction.
+__device__ __forceinline__ float ex2_approx(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float lg2_approx(float x)
+{
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ uint64_t globaltimer()
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ float clampf(float v, float lim) { return fminf(fmaxf(v, -lim), lim); }
+
+__device__ __forceinline__ uint32_t bit_of(const uint32_t *words, int i) { return (words[i >> 5] >> (i & 31)) & 1u; }
+
+// Device copy of pc_code_t (same layout; kernels take it by value).
+struct Code {
+    int32_t N, n, k, m, crc_width;
+    uint32_t crc_offset, enc_crc_offset;
+    const uint32_t *frozen_bits, *crc_cols;
+    const int32_t *info_pos;
+    const uint32_t *enc_cols, *da_bits;
+};
+
+inline Code to_device_code(const pc_code_t &c)
+{
+    Code d;
+    d.N = c.N;
+    d.n = c.n;
+    d.k = c.k;
+    d.m = c.m;
+    d.crc_width = c.crc_width;
+    d.crc_offset = c.crc_offset;
+    d.enc_crc_offset = c.enc_crc_offset;
+    d.frozen_bits = c.frozen_bits;
+    d.crc_cols = c.crc_cols;
+    d.info_pos = c.info_pos;
+    d.enc_cols = c.enc_cols;
+    d.da_bits = c.da_bits;
+    return d;
+}
+
+} // namespace pc

@@ -1,0 +1,177 @@
+"""K1 (pc_bp_decode / pc_bp_iterate) parity against the fp64 oracle and the
+reference's golden outputs.
+
+Tolerances (fp32 device vs fp64 reference, SURVEY.md section 7 hard parts 1-2):
+* teacher-forced messages: |d| / max(|ref|, 1) <= 1e-4 after one iteration
+  from identical state;
+* decisions with the CRC stop: converged flag, iteration count and u_hat
+  identical on every frame the reference decides within 20 iterations (the
+  fp32/fp64 divergence horizon); later frames are the documented near-tie
+  class and may differ in at most 2% of a set (listed when they do).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden_frames, unpack
+from paper_1609_09358_b200 import BpConfig, CodeConfig, bp_decode, bp_decode_batch, init_graph, iterate_once
+from paper_1609_09358_b200.channel import channel_llr, ebno_to_sigma, frame_rng, make_frame, modulate_bpsk
+from paper_1609_09358_b200.codes import insert_message, polar_transform
+
+pytestmark = pytest.mark.gpu
+
+MSG_TOL = 1e-4
+NEAR_TIE_ITERS = 20
+
+
+def mixed_err(a, b):
+    return np.max(np.abs(a - b) / np.maximum(np.abs(b), 1.0))
+
+
+@pytest.mark.parametrize("N", [32, 1024])
+def test_teacher_forced_iteration_matches_reference(golden, N):
+    code = CodeConfig(N, N // 2, crc=None)
+    g = BpGraph_from(golden[f"tf{N}_lin"], golden[f"tf{N}_rin"])
+    iterate_once(g, code, BpConfig(stop_mode="none"))
+    assert mixed_err(g.l_msgs, golden[f"tf{N}_lout"]) <= MSG_TOL
+    assert mixed_err(g.r_msgs, golden[f"tf{N}_rout"]) <= MSG_TOL
+
+
+def BpGraph_from(L, R):
+    from paper_1609_09358_b200 import BpGraph
+
+    return BpGraph(np.array(L, dtype=np.float64), np.array(R, dtype=np.float64))
+
+
+@pytest.mark.parametrize("N,g_mode", [(4, "exact"), (8, "min"), (128, "exact"), (128, "min"), (2048, "exact")])
+def test_teacher_forced_iterations_vs_oracle(N, g_mode):
+    """Five iterations, each restarted from the oracle's own state (teacher forcing)."""
+    code = CodeConfig(N, N // 2, crc=None)
+    cfg = BpConfig(g_mode=g_mode, stop_mode="none")
+    rng = frame_rng(5, 0, N)
+    _, llr = make_frame(code, ebno_to_sigma(1.5, code.rate), rng)
+    g = init_graph(llr.astype(np.float32).astype(np.float64), code, cfg)
+    L, R = g.l_msgs, g.r_msgs
+    for _ in range(5):
+        L = L.astype(np.float32).astype(np.float64)
+        R = R.astype(np.float32).astype(np.float64)
+        ref_L, ref_R = oracle.bp_iterate(L, R, g_mode)
+        dev = BpGraph_from(L, R)
+        iterate_once(dev, code, cfg)
+        assert mixed_err(dev.l_msgs, ref_L) <= MSG_TOL
+        assert mixed_err(dev.r_msgs, ref_R) <= MSG_TOL
+        assert np.abs(dev.l_msgs).max() <= cfg.llr_max and np.abs(dev.r_msgs).max() <= cfg.llr_max
+        L, R = ref_L, ref_R
+
+
+def _check_decisions(name, ref_u, ref_it, ref_cv, got):
+    """Flags and iteration counts must agree; u_hat must agree where both converged.
+
+    A non-converged frame's u_hat is the chaotic state after i_max iterations
+    (the hybrid discards it), so it is not compared.  Flag/iteration flips are
+    allowed only on near-tie frames (reference iterations > 20) and at most 2%.
+    """
+    u = got.u_hat
+    bad_early, late = [], []
+    for f in range(len(ref_it)):
+        same = bool(got.converged[f]) == bool(ref_cv[f]) and int(got.iterations_used[f]) == int(ref_it[f])
+        if same and ref_cv[f]:
+            same = np.array_equal(u[f], ref_u[f])
+        if not same:
+            (bad_early if ref_it[f] <= NEAR_TIE_ITERS else late).append((f, int(ref_it[f]), int(got.iterations_used[f])))
+    assert not bad_early, f"{name}: frames decided within {NEAR_TIE_ITERS} iterations differ: {bad_early}"
+    assert len(late) <= max(2, int(0.02 * len(ref_it))), f"{name}: near-tie flips {late}"
+    both = np.asarray(got.converged, bool) & np.asarray(ref_cv, bool)
+    assert all(np.array_equal(u[f], ref_u[f]) for f in np.flatnonzero(both)), f"{name}: u_hat differs on converged frames"
+    return late
+
+
+@pytest.mark.parametrize("name", ["bp128", "bp1024a", "bp1024b", "bp2048"])
+def test_crc_stop_decisions_match_reference(golden, golden_meta, name):
+    meta = golden_meta["sets"][name]
+    code = CodeConfig(meta["N"], meta["k"], crc=16)
+    _, llrs = golden_frames(meta, code)
+    got = bp_decode_batch(llrs, code, BpConfig(i_max=50, stop_mode="crc"))
+    late = _check_decisions(name, unpack(golden[f"{name}_u"], code.N), golden[f"{name}_iters"],
+                            golden[f"{name}_conv"], got)
+    if late:
+        print(f"{name}: documented near-tie frames {late}")
+
+
+@pytest.mark.parametrize("mode", ["reencode", "none"])
+def test_other_stop_modes_match_reference(golden, golden_meta, mode):
+    meta = golden_meta["sets"]["bp64"]
+    code = CodeConfig(64, 32, crc=None)
+    _, llrs = golden_frames(meta, code)
+    got = bp_decode_batch(llrs, code, BpConfig(i_max=20, stop_mode=mode))
+    ref_it = golden[f"bp64_{mode}_iters"]
+    ref_cv = golden[f"bp64_{mode}_conv"]
+    assert np.array_equal(got.converged, ref_cv.astype(bool))
+    assert np.array_equal(got.iterations_used, ref_it)
+    if mode == "reencode":
+        ref_u = unpack(golden[f"bp64_{mode}_u"], 64)
+        for f in np.flatnonzero(ref_cv):
+            assert np.array_equal(got.u_hat[f], ref_u[f])
+
+
+def test_crc_stop_vs_oracle_at_scale():
+    """2000 frames N=1024 at 2 dB against the C oracle on identical fp32 inputs."""
+    code = CodeConfig(1024, 512, crc=16)
+    sigma = ebno_to_sigma(2.0, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(404, 0, f))[1] for f in range(2000)])
+    llrs = llrs.astype(np.float32).astype(np.float64)
+    ref_u, ref_it, ref_cv = oracle.bp_batch(llrs, code, stop_mode="crc")
+
+    got = bp_decode_batch(llrs, code, BpConfig(i_max=50, stop_mode="crc"))
+    late = _check_decisions("oracle2000", ref_u, ref_it, ref_cv, got)
+    print("near-tie frames:", late)
+
+
+def test_single_frame_api_and_soft_outputs():
+    code = CodeConfig(128, 64, crc=16)
+    sigma = ebno_to_sigma(2.0, code.rate)
+    msg, llr = make_frame(code, sigma, frame_rng(8, 0, 3))
+    llr = llr.astype(np.float32).astype(np.float64)
+    res = bp_decode(llr, code, BpConfig(stop_mode="crc"))
+    ref = oracle.bp_decode(llr, code, stop_mode="crc")
+    assert res.converged == ref["converged"] and res.iterations_used == ref["iterations_used"]
+    assert np.array_equal(res.u_hat, ref["u_hat"])
+    assert mixed_err(res.soft_u, ref["soft_u"]) <= 1e-3
+    assert mixed_err(res.soft_x, ref["soft_x"]) <= 1e-3
+    assert np.array_equal(res.x_hat, (ref["soft_x"] < 0).astype(np.uint8))
+
+
+def test_noiseless_converges_within_n_iterations():
+    rng = np.random.default_rng(35)
+    for N, k in ((8, 4), (64, 32), (1024, 512)):
+        code = CodeConfig(N, k, crc=None)
+        msgs = rng.integers(0, 2, (20, k)).astype(np.uint8)
+        x = np.array([polar_transform(insert_message(m, code)) for m in msgs])
+        llrs = channel_llr(modulate_bpsk(x), 0.0)
+        got = bp_decode_batch(llrs, code, BpConfig(stop_mode="reencode"))
+        assert got.converged.all()
+        assert (got.iterations_used <= code.n).all()
+        assert np.array_equal(got.u_hat[:, code.info_positions], msgs)
+
+
+@pytest.mark.parametrize("tpf", [64, 128, 256, 512])
+def test_threads_per_frame_variants_agree(tpf):
+    code = CodeConfig(1024, 512, crc=16)
+    sigma = ebno_to_sigma(2.5, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(9, 0, f))[1] for f in range(64)])
+    from paper_1609_09358_b200 import _native as nat
+    import torch
+
+    x = torch.from_numpy(llrs.astype(np.float32)).cuda()
+    base = bp_decode_batch(x, code, BpConfig(stop_mode="crc"))
+    import ctypes
+
+    cfg = BpConfig(stop_mode="crc").native(threads_per_frame=tpf)
+    dc = nat.device_code(code)
+    u = torch.empty_like(base.u_hat)
+    it = torch.empty_like(base.iterations_used)
+    cv = torch.empty(64, dtype=torch.uint8, device="cuda")
+    nat.check(nat.load().pc_bp_decode(x.data_ptr(), 64, dc.ref, ctypes.byref(cfg), u.data_ptr(), None, None, None,
+                                      it.data_ptr(), cv.data_ptr(), None, nat.stream_handle()), "bp")
+    assert torch.equal(u, base.u_hat) and torch.equal(it, base.iterations_used)
