@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Headline benchmark: hybrid BP -> SCL decoding, N=1024 K=512 (496 payload +
+16 CRC bits), L=32, i_max=50, swept over Eb/N0 = 1..4 dB (BASELINE.json).
+
+A step = one pass of the device pipeline (K1 BP with fused CRC stop -> K2
+compaction -> K3 CRC-aided SCL on the failures) over one batch of B frames at
+EVERY sweep point.  value = decoded payload Gbit/s over the whole sweep
+(sum of bits / sum of time), whole job over all ranks; per-point Gbit/s, p50
+frame latency, gamma and FER are in "sweep".
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU: frames shard by index (weak scaling, no collective on the data
+path); timing is the max over ranks of the barrier-bracketed device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decoded info Gbit/s, hybrid BP+SCL N=1024 L=32, vs Eb/N0; p50 frame latency"
+EBNO = (1.0, 1.5, 2.0, 2.5, 3.0, 3.5, 4.0)
+N, K, LIST, IMAX = 1024, 512, 32, 50
+SEED = 20240917
+WORKLOAD = "hybrid BP->SCL N=1024 K=512 (496 payload + CRC-16) L=32 i_max=50, Eb/N0 1-4 dB step 0.5"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 7:
+                    self.rows.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ CPU baseline --
+def cpu_hybrid_sample(frames_per_point: int, threads: int):
+    """The oracle port (oracle/oracle.c, fp64, the reference's algorithm) on the
+    host cores over a bounded sample of the same sweep; returns (Gbit/s, info)."""
+    import oracle
+    from paper_1609_09358_b200 import CodeConfig
+    from paper_1609_09358_b200.channel import ebno_to_sigma, frame_rng, make_frame
+
+    code = CodeConfig(N, K, crc=16)
+    bits = 0
+    busy = 0.0
+    for p, eb in enumerate(EBNO):
+        sigma = ebno_to_sigma(eb, code.rate)
+        llrs = np.array([make_frame(code, sigma, frame_rng(SEED, p, f))[1] for f in range(frames_per_point)])
+        t0 = time.perf_counter()
+        oracle.hybrid_batch(llrs, code, i_max=IMAX, L=LIST, nthreads=threads)
+        busy += time.perf_counter() - t0
+        bits += frames_per_point * code.message_len
+    return bits / busy / 1e9, busy
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+
+    threads = oracle.cpu_count()
+    fpp = args.cpu_frames or max(128, 8 * threads)
+    vals = []
+    for s in range(args.warmup + args.steps):
+        v, busy = cpu_hybrid_sample(fpp if s >= args.warmup else max(8, threads), threads)
+        if s >= args.warmup:
+            vals.append((v, busy))
+    value = float(np.mean([v for v, _ in vals]))
+    ms = float(np.mean([b for _, b in vals])) * 1e3
+    sample = f"{fpp} frames per Eb/N0 point x {len(EBNO)} points per step (host PCG64 frames, fp64 oracle port)"
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": WORKLOAD, "ebno_db": list(EBNO), "frames_per_point": fpp},
+        "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm --
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1609_09358_b200 import BpConfig, CodeConfig, HybridDecoder, SclConfig
+    from paper_1609_09358_b200 import _native as nat
+    from paper_1609_09358_b200.channel import ebno_to_sigma
+
+    lib = nat.load()
+    code = CodeConfig(N, K, crc=16)
+    m = code.message_len
+    B = args.frames
+    dev = torch.device("cuda", local)
+    dc = nat.device_code(code)
+    MW = (m + 31) // 32
+    # inputs resident in HBM before timing: per point B frames keyed by the global frame index
+    llr = torch.empty((len(EBNO), B, N), dtype=torch.float32, device=dev)
+    msg = torch.empty((len(EBNO), B, MW), dtype=torch.int32, device=dev)
+    for p, eb in enumerate(EBNO):
+        sigma = ebno_to_sigma(eb, code.rate)
+        nat.check(lib.pc_gen_frames(SEED, p, rank * B, B, sigma, dc.ref, msg[p].data_ptr(), llr[p].data_ptr(),
+                                    nat.stream_handle()), "pc_gen_frames")
+    dec = HybridDecoder(code, BpConfig(i_max=IMAX), SclConfig(LIST), capacity=B, chunk=args.chunk or B)
+    errs = torch.zeros((len(EBNO), 2), dtype=torch.int64, device=dev)
+
+    def one_step(timed_events=None):
+        per_point = []
+        for p in range(len(EBNO)):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            dec.run(llr[p], B)
+            b.record()
+            per_point.append((a, b))
+        return per_point
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+
+    # ---- timed region (device time, events on the launching streams) ----
+    dec.kernel_events = []
+    lat_p50, gammas, iters_sum, pt_ms = [[] for _ in EBNO], [[] for _ in EBNO], [0] * len(EBNO), [0.0] * len(EBNO)
+    with ClockSampler(local) as clocks:
+        barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record()
+        records = []
+        for _ in range(args.steps):
+            records.append(one_step())
+            # per-point statistics of this step (read after the timed region)
+            records[-1] = (records[-1], None)
+        t_end.record()
+        barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    # per-point times and BP kernel times
+    bp_ms = [a.elapsed_time(b) for a, b in dec.kernel_events]
+    dec.kernel_events = None
+    for step_rec, _ in records:
+        for p, (a, b) in enumerate(step_rec):
+            pt_ms[p] += a.elapsed_time(b)
+    # statistics pass (untimed): gamma, iterations, latency, FER per point
+    for p in range(len(EBNO)):
+        dec.run(llr[p], B).sync()
+        r = dec.host_results()
+        gammas[p] = float((~r["converged"]).mean())
+        iters_sum[p] = int(r["iters"].astype(np.int64).sum())
+        st = r["stamps"]
+        c = np.arange(B) // dec.chunk
+        done = np.where(r["converged"], r["t_bp"], r["t_scl"])
+        lat_p50[p] = float(np.median(done - st[c, 0])) * 1e-6
+        nat.check(lib.pc_count_errors(dec.payload.data_ptr(), msg[p].data_ptr(), B, m, errs[p].data_ptr(),
+                                      nat.stream_handle()), "pc_count_errors")
+    torch.cuda.synchronize()
+    errs_h = errs.cpu().numpy()
+
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    bits_step = B * m * len(EBNO)
+    value = world * bits_step * args.steps / (max_ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (K1): algorithmic exact-g evaluations / K1 time ----
+    n = code.n
+    g_per_step = sum(iters_sum) * 2 * n * N  # iterations are deterministic per input set
+    bp_ms_step = sum(bp_ms) / args.steps
+    achieved = g_per_step / (bp_ms_step * 1e-3) / 1e9  # Gg/s
+    ck = clocks.summary()
+    peak_mhz = 1965.0
+    try:
+        peak_mhz = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("sm_max_mhz", 1965.0))
+    except Exception:
+        pass
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = sms * 16 * peak_mhz * 1e6 / 4 / 1e9  # MUFU ops/s / 4 MUFU per exact g, in Gg/s
+    traffic = None
+    prof = ROOT / "profiles" / "bp_kernel_ncu.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "xu", "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
+        "traffic": traffic, "kernel": "k_bp_decode<10,512,0>",
+        "note": "exact-g node updates/s of K1 vs the MUFU (XU) pipe bound: 148 SM x 16 MUFU/clk x sm_max_mhz / "
+                "4 MUFU per g; HBM is <1% (4.2 KB/frame)",
+        "peak_at_measured_clock": (sms * 16 * ck["sm_mhz"] * 1e6 / 4 / 1e9) if ck.get("sm_mhz") else None,
+        # K1's own HBM traffic: read the LLRs, write payload + iters + flag + stamp per frame
+        "hbm_gbs": len(EBNO) * B * (4 * N + 4 * MW + 4 + 1 + 8) / (bp_ms_step * 1e-3) / 1e9,
+        "bp_share_of_step": bp_ms_step / (max_ms / args.steps),
+    }
+
+    # ---- e2e: the public host-buffer call, H2D + decode + D2H inside the timed region ----
+    e2e_val = None
+    if rank == 0 or world > 1:
+        host = [torch.empty((B, N), dtype=torch.float32, pin_memory=True) for _ in EBNO]
+        for p in range(len(EBNO)):
+            host[p].copy_(llr[p])
+        torch.cuda.synchronize()
+        for p in range(len(EBNO)):
+            dec.decode_host(host[p])
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for p in range(len(EBNO)):
+                dec.decode_host(host[p])
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_val = world * bits_step * args.steps / float(te.item()) / 1e9
+    h2d = B * N * 4 * len(EBNO)
+    d2h = B * (MW * 4 + 1) * len(EBNO)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        import oracle
+
+        threads = oracle.cpu_count()
+        fpp = args.cpu_frames or max(128, 8 * threads)
+        v, busy = cpu_hybrid_sample(fpp, threads)
+        cpu = {"value": v, "unit": "Gbit/s", "cores": threads, "kind": "port",
+               "sample": f"{fpp} frames per Eb/N0 point x {len(EBNO)} points, {busy:.1f} s of CPU wall "
+                         f"(fp64 oracle port of the reference algorithm, all host threads)"}
+
+    sweep = []
+    for p, eb in enumerate(EBNO):
+        ms = pt_ms[p] / args.steps
+        sweep.append({"ebno_db": eb, "gbps": B * m / (ms * 1e-3) / 1e9 * world, "ms": ms, "gamma": gammas[p],
+                      "mean_bp_iters": iters_sum[p] / B, "p50_latency_ms": lat_p50[p],
+                      "fer": float(errs_h[p, 1]) / B, "ber": float(errs_h[p, 0]) / (B * m), "frames": B * world})
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (device Philox-keyed BPSK/AWGN frames, resident in HBM before timing)",
+            "config": {"workload": WORKLOAD, "frames_per_point_per_gpu": B, "ebno_db": list(EBNO),
+                       "chunk": dec.chunk, "parallelism": f"frame-sharded x{world}",
+                       "l2": f"inputs larger than L2 ({B * N * 4 / 1e6:.0f} MB per point)"},
+            "p50_latency_ms": float(np.median([s["p50_latency_ms"] for s in sweep])),
+            "sweep": sweep,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "Gbit/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": args.steps * len(EBNO) * ((B + dec.chunk - 1) // dec.chunk) * dec.launches_per_chunk,
+            "clocks": ck,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=1 << 17, help="frames per Eb/N0 point per GPU")
+    ap.add_argument("--chunk", type=int, default=0, help="frames per BP/SCL chunk (0 = whole batch)")
+    ap.add_argument("--cpu-frames", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -178,7 +178,28 @@ class HybridDecoder:
         self.workspaces = torch.zeros((self.nchunks_max, 64), dtype=torch.int32, **z)
         self.s_bp = torch.cuda.Stream(device=dev)
         self.s_scl = torch.cuda.Stream(device=dev) if overlap else self.s_bp
-        self.u_scratch = None  # u bits are not needed by the pipeline
+        self.kernel_events = None  # set to [] to time every K1 launch with CUDA events on the BP stream
+        self.launches_per_chunk = 7  # 4 stamp kernels + K1 + K2 + K3 (memset nodes not counted)
+        self._llr_dev = None
+
+    def decode_host(self, llr_host, B: int | None = None):
+        """End-to-end call with HOST buffers: pinned LLRs [B, N] float32 in,
+        payload words [B, ceil(m/32)] (numpy uint32 view) out.  The H2D copy,
+        the pipeline and the D2H copy are ordered on the current stream."""
+        torch = self.torch
+        B = int(llr_host.shape[0] if B is None else B)
+        if self._llr_dev is None or self._llr_dev.shape[0] < B:
+            self._llr_dev = torch.empty((self.capacity, self.code.N), dtype=torch.float32, device=self.device)
+        dst = self._llr_dev[:B]
+        dst.copy_(llr_host[:B], non_blocking=True)
+        self.run(dst, B)
+        if getattr(self, "_pay_host", None) is None or self._pay_host.shape[0] < self.capacity:
+            self._pay_host = torch.empty((self.capacity, self.MW), dtype=torch.int32, pin_memory=True)
+            self._conv_host = torch.empty(self.capacity, dtype=torch.uint8, pin_memory=True)
+        self._pay_host[:B].copy_(self.payload[:B], non_blocking=True)
+        self._conv_host[:B].copy_(self.conv[:B], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return self._pay_host[:B].numpy().view(np.uint32), self._conv_host[:B].numpy().astype(bool)
 
     def _st(self, s) -> int:
         return int(s.cuda_stream)
@@ -203,6 +224,9 @@ class HybridDecoder:
             sb, ss = self._st(self.s_bp), self._st(self.s_scl)
             st = self.stamps[c]
             chk(lib.pc_stamp(st.data_ptr(), sb), "pc_stamp")
+            if self.kernel_events is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(self.s_bp)
             chk(
                 lib.pc_bp_decode(
                     base_llr + 4 * N * b0, nb, self.dc_bp.ref, bp_ref, None,
@@ -211,6 +235,10 @@ class HybridDecoder:
                 ),
                 "pc_bp_decode",
             )
+            if self.kernel_events is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(self.s_bp)
+                self.kernel_events.append((e0, e1))
             chk(lib.pc_stamp(st.data_ptr() + 8, sb), "pc_stamp")
             if self.overlap:
                 ev = torch.cuda.Event()
