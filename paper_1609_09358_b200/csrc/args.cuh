@@ -34,7 +34,8 @@ struct SclArgs {
     int32_t ss;      // LLR slot stride (floats)
     int32_t psw;     // partial-sum slot stride (words)
     int32_t uhs;     // decision slot stride (words)
-    int32_t warp_words;
+    int32_t warp_words;  // per-warp shared words (slots, partial sums, decisions, candidates, channel)
+    int32_t table_words; // CTA-shared frozen / decision-aided masks
 };
 
 int launch_bp_decode(const BpArgs &a, int g_mode, int tpf, cudaStream_t s);

@@ -14,31 +14,34 @@
 // Mapping (B200-first, not the reference's loop nest):
 //   * one WARP decodes F = 32 / L frames; lane = (frame group, path) and the
 //     lane index IS the physical slot of that logical path.  Every f/g level
-//     is a per-lane loop over that path's elements, so the whole decoder runs
-//     with __syncwarp only -- no CTA barriers, 32 paths in SIMT lock-step;
+//     is a per-lane loop over that path's elements (float4 shared-memory
+//     traffic), so the decoder synchronises with __syncwarp only -- no CTA
+//     barriers, L paths in SIMT lock-step;
 //   * path copies are LAZY: each lane keeps, in two 64-bit registers, a 5-bit
 //     slot pointer per tree level (LLR levels and partial-sum levels).  A
-//     clone copies its parent's pointers (two shuffles) instead of the data;
+//     clone copies its parent's pointers (shuffles) instead of the data;
 //     writes always go to the lane's own slot.  Because all paths rewrite the
 //     same levels at the same bit index, a level is never overwritten while
-//     another path still points to it (see DESIGN.md, "SCL lazy copies");
-//   * the top `NV` tree levels are not stored: they are recomputed from the
-//     channel LLRs when the highest stored level needs them, which cuts shared
-//     memory per warp (and raises warps per SM) at a small FMA cost;
-//   * survivor selection is a pairwise rank count over the group's 2L
-//     candidates with warp shuffles; slot assignment uses ballots.
+//     another path still points to it (DESIGN.md, "SCL lazy copies");
+//   * the top NV tree levels are not stored but recomputed from the channel
+//     LLRs (kept in shared memory for L >= 16) when the highest stored level
+//     needs them: less shared memory per warp, more warps per SM;
+//   * survivor selection: when every path's agreeing child beats every
+//     disagreeing child (the common case at reliable positions) the survivors
+//     are known after two warp reductions; otherwise a rank count over the
+//     group's 2L candidates broadcast from shared memory, with an exact
+//     (metric, index) pass only when the group holds tied metrics.
 #include "args.cuh"
 
 namespace pc {
 
-
+// _kernels.py:40-48.  When either input is zero the magnitude is zero; the
+// sign bit of that zero is irrelevant downstream (f, g, the metric and the
+// hard decision treat -0 and +0 alike).
 __device__ __forceinline__ float f_minsum(float a, float b)
 {
-    // _kernels.py:40-48: zero if either input is zero, else sign * min
-    float mag = fminf(fabsf(a), fabsf(b));
-    if ((a < 0.0f) != (b < 0.0f))
-        mag = -mag;
-    return (a == 0.0f || b == 0.0f) ? 0.0f : mag;
+    const float mag = fminf(fabsf(a), fabsf(b));
+    return __uint_as_float(__float_as_uint(mag) | ((__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u));
 }
 
 __device__ __forceinline__ float f_boxplus(float a, float b)
@@ -56,27 +59,34 @@ __device__ __forceinline__ float scl_f(float a, float b)
     return FEX ? f_boxplus(a, b) : f_minsum(a, b);
 }
 
-__device__ __forceinline__ float scl_g(float a, float b, uint32_t u) { return u ? b - a : b + a; }
+// _kernels.py:68-73: b + (1 - 2u) a  (b - a == b + (-a) exactly in IEEE)
+__device__ __forceinline__ float scl_g(float a, float b, uint32_t u)
+{
+    return b + __uint_as_float(__float_as_uint(a) ^ (u << 31));
+}
 
 // Metric increments for both decisions at soft value lam (_kernels.py:76-90).
 __device__ __forceinline__ void metric_incs(float lam, bool exact, float &inc0, float &inc1)
 {
     if (exact) {
+        // sp = log1p(exp(-|lam|)) on the MUFU pipe: ex2 then lg2(1 + e); for
+        // e < 2^-10 the two-term series e (1 - e/2) is more accurate than lg2
+        // of a value that close to 1.  Absolute error < 2e-7, below the fp32
+        // rounding of the metrics it is added to.
         const float y = fabsf(lam);
-        const float sp = log1pf(expf(-y));
+        const float e = ex2_approx(-y * PC_LOG2E);
+        const float sp = e < 0.0009765625f ? e * (1.0f - 0.5f * e) : PC_LN2 * lg2_approx(1.0f + e);
         const float agree = sp, disagree = y + sp;
         // x = lam for u = 0: x > 0 -> sp(x); x <= 0 -> -x + sp(-x)
         inc0 = lam > 0.0f ? agree : disagree;
         inc1 = lam < 0.0f ? agree : disagree;
-        if (lam == 0.0f)
-            inc0 = inc1 = sp;
     } else {
         inc0 = lam < 0.0f ? -lam : 0.0f;
         inc1 = lam > 0.0f ? lam : 0.0f;
     }
 }
 
-// word offset of partial-sum level s: levels < 5 take one word, level s >= 5 takes 2^(s-5)
+// word offset of partial-sum level s: levels <= 5 take one word, level s > 5 takes 2^(s-5)
 __host__ __device__ __forceinline__ int ps_off(int s) { return s <= 5 ? s : (1 << (s - 5)) + 4; }
 
 __device__ __forceinline__ int slot_of(uint64_t ptrs, int s) { return (int)((ptrs >> (5 * s)) & 31u); }
@@ -85,238 +95,411 @@ __device__ __forceinline__ uint64_t set_slot(uint64_t ptrs, int s, int v)
     return (ptrs & ~(31ull << (5 * s))) | ((uint64_t)v << (5 * s));
 }
 
-// Per-lane view of the tree: pointer registers and the recomputed top levels.
-struct Tree {
-    const float *ch;    // channel LLRs of this lane's frame
-    const uint32_t *ps; // warp partial-sum slots
-    int n, i, psw;
-    uint64_t pl, pp; // pointer registers (llr levels, partial-sum levels)
+__device__ __forceinline__ uint32_t bitw(const uint32_t *p, int x) { return (p[x >> 5] >> (x & 31)) & 1u; }
 
-    __device__ __forceinline__ uint32_t psbit(int s, int t) const
-    {
-        return (ps[slot_of(pp, s) * psw + ps_off(s) + (t >> 5)] >> (t & 31)) & 1u;
-    }
-
-    // Recompute element t of the highest virtual level s = n - NV from the
-    // 2^NV channel leaves t + j 2^s (bottom-up, registers only).
-    template <int NV, bool FEX>
-    __device__ __forceinline__ float virt(int t) const
-    {
-        static_assert(NV >= 1 && NV <= 4, "virtual levels");
-        constexpr int CNT = 1 << (NV - 1);
-        const int s = n - NV;
-        const int half = 1 << (n - 1);
-        float v[CNT];
-        const bool g_top = (i >> (n - 1)) & 1;
+// Element t of the highest virtual level s = n - NV, recomputed bottom-up from
+// the 2^NV channel leaves t + j 2^s.  psp[d] = partial-sum words of level s+d,
+// bit d of gmask = the op at level s+d is g.
+template <int NV, bool FEX>
+__device__ __forceinline__ float virt_top(const float *ch, int n, int t, const uint32_t *const *psp, uint32_t gmask)
+{
+    constexpr int CNT = 1 << (NV - 1);
+    const int s = n - NV;
+    const int half = 1 << (n - 1);
+    float v[CNT];
 #pragma unroll
-        for (int j = 0; j < CNT; ++j) {
+    for (int j = 0; j < CNT; ++j) {
+        const int x = t + (j << s);
+        const float A = ch[x], B = ch[x + half];
+        v[j] = ((gmask >> (NV - 1)) & 1u) ? scl_g(A, B, bitw(psp[NV - 1], x)) : scl_f<FEX>(A, B);
+    }
+#pragma unroll
+    for (int d = NV - 2; d >= 0; --d) {
+        const int c = 1 << d;
+#pragma unroll
+        for (int j = 0; j < c; ++j) {
             const int x = t + (j << s);
-            const float A = __ldg(ch + x), B = __ldg(ch + x + half);
-            v[j] = g_top ? scl_g(A, B, psbit(n - 1, x)) : scl_f<FEX>(A, B);
+            v[j] = ((gmask >> d) & 1u) ? scl_g(v[j], v[j + c], bitw(psp[d], x)) : scl_f<FEX>(v[j], v[j + c]);
         }
-#pragma unroll
-        for (int d = NV - 2; d >= 0; --d) { // level r = s + d, d counts down to s
-            const int r = s + d;
-            const int c = 1 << d;
-            const bool g = (i >> r) & 1;
-#pragma unroll
-            for (int j = 0; j < c; ++j) {
-                const int x = t + (j << s);
-                v[j] = g ? scl_g(v[j], v[j + c], psbit(r, x)) : scl_f<FEX>(v[j], v[j + c]);
-            }
-        }
-        return v[0];
     }
-};
+    return v[0];
+}
+
+__device__ __forceinline__ float4 f4(const float4 A, const float4 B, bool fex)
+{
+    float4 o;
+    if (fex) {
+        o.x = f_boxplus(A.x, B.x);
+        o.y = f_boxplus(A.y, B.y);
+        o.z = f_boxplus(A.z, B.z);
+        o.w = f_boxplus(A.w, B.w);
+    } else {
+        o.x = f_minsum(A.x, B.x);
+        o.y = f_minsum(A.y, B.y);
+        o.z = f_minsum(A.z, B.z);
+        o.w = f_minsum(A.w, B.w);
+    }
+    return o;
+}
+
+__device__ __forceinline__ float4 g4(const float4 A, const float4 B, uint32_t bits)
+{
+    return make_float4(scl_g(A.x, B.x, bits & 1u), scl_g(A.y, B.y, (bits >> 1) & 1u), scl_g(A.z, B.z, (bits >> 2) & 1u),
+                       scl_g(A.w, B.w, (bits >> 3) & 1u));
+}
+
+// Vector form of virt_top: elements t..t+3 (t % 4 == 0) of the highest
+// virtual level; one partial-sum word serves all four elements.
+template <int NV, bool FEX>
+__device__ __forceinline__ float4 virt_top4(const float *ch, int n, int t, const uint32_t *const *psp, uint32_t gmask)
+{
+    constexpr int CNT = 1 << (NV - 1);
+    const int s = n - NV;
+    const int half = 1 << (n - 1);
+    float4 v[CNT];
+#pragma unroll
+    for (int j = 0; j < CNT; ++j) {
+        const int x = t + (j << s);
+        const float4 A = *reinterpret_cast<const float4 *>(ch + x);
+        const float4 B = *reinterpret_cast<const float4 *>(ch + x + half);
+        v[j] = ((gmask >> (NV - 1)) & 1u) ? g4(A, B, psp[NV - 1][x >> 5] >> (x & 31)) : f4(A, B, FEX);
+    }
+#pragma unroll
+    for (int d = NV - 2; d >= 0; --d) {
+        const int c = 1 << d;
+#pragma unroll
+        for (int j = 0; j < c; ++j) {
+            const int x = t + (j << s);
+            v[j] = ((gmask >> d) & 1u) ? g4(v[j], v[j + c], psp[d][x >> 5] >> (x & 31)) : f4(v[j], v[j + c], FEX);
+        }
+    }
+    return v[0];
+}
+
+// One stored level s (width w = 2^s) from a stored source level (src points at
+// its first element), f or g with partial sums pw.
+template <bool FEX, bool G>
+__device__ __forceinline__ void level_from(float *__restrict__ dst, const float *__restrict__ src, int w,
+                                           const uint32_t *__restrict__ pw)
+{
+    if (w >= 4) {
+#pragma unroll 2
+        for (int t = 0; t < w; t += 4) {
+            const float4 A = *reinterpret_cast<const float4 *>(src + t);
+            const float4 B = *reinterpret_cast<const float4 *>(src + w + t);
+            float4 o;
+            if (G) {
+                const uint32_t bits = pw[t >> 5] >> (t & 31);
+                o.x = scl_g(A.x, B.x, bits & 1u);
+                o.y = scl_g(A.y, B.y, (bits >> 1) & 1u);
+                o.z = scl_g(A.z, B.z, (bits >> 2) & 1u);
+                o.w = scl_g(A.w, B.w, (bits >> 3) & 1u);
+            } else {
+                o.x = scl_f<FEX>(A.x, B.x);
+                o.y = scl_f<FEX>(A.y, B.y);
+                o.z = scl_f<FEX>(A.z, B.z);
+                o.w = scl_f<FEX>(A.w, B.w);
+            }
+            *reinterpret_cast<float4 *>(dst + t) = o;
+        }
+    } else {
+        const uint32_t bits = G ? pw[0] : 0u;
+        for (int t = 0; t < w; ++t)
+            dst[t] = G ? scl_g(src[t], src[w + t], (bits >> t) & 1u) : scl_f<FEX>(src[t], src[w + t]);
+    }
+}
+
+// Levels s..0 (s <= 2) in registers from source level s+1 at `src` (op at
+// level s is g when `g`, with partial-sum bits `bits`; f below).  Stores the
+// levels into the own slot (they are read again by later g steps and clones)
+// and returns the level-0 soft value without reloading it.
+template <bool FEX>
+__device__ __forceinline__ float tail_from(float *own, const float *src, int s, uint32_t g, uint32_t bits)
+{
+    float l1a, l1b;
+    if (s == 2) {
+        const float4 A = *reinterpret_cast<const float4 *>(src);
+        const float4 B = *reinterpret_cast<const float4 *>(src + 4);
+        float4 o;
+        if (g) {
+            o.x = scl_g(A.x, B.x, bits & 1u);
+            o.y = scl_g(A.y, B.y, (bits >> 1) & 1u);
+            o.z = scl_g(A.z, B.z, (bits >> 2) & 1u);
+            o.w = scl_g(A.w, B.w, (bits >> 3) & 1u);
+        } else {
+            o.x = scl_f<FEX>(A.x, B.x);
+            o.y = scl_f<FEX>(A.y, B.y);
+            o.z = scl_f<FEX>(A.z, B.z);
+            o.w = scl_f<FEX>(A.w, B.w);
+        }
+        *reinterpret_cast<float4 *>(own + 4) = o;
+        l1a = scl_f<FEX>(o.x, o.z);
+        l1b = scl_f<FEX>(o.y, o.w);
+    } else if (s == 1) {
+        const float4 v = *reinterpret_cast<const float4 *>(src);
+        l1a = g ? scl_g(v.x, v.z, bits & 1u) : scl_f<FEX>(v.x, v.z);
+        l1b = g ? scl_g(v.y, v.w, (bits >> 1) & 1u) : scl_f<FEX>(v.y, v.w);
+    } else {
+        const float2 v = *reinterpret_cast<const float2 *>(src);
+        const float lam = g ? scl_g(v.x, v.y, bits & 1u) : scl_f<FEX>(v.x, v.y);
+        own[1] = lam;
+        return lam;
+    }
+    *reinterpret_cast<float2 *>(own + 2) = make_float2(l1a, l1b);
+    const float lam = scl_f<FEX>(l1a, l1b);
+    own[1] = lam;
+    return lam;
+}
 
 template <int L, bool FEX, int NV>
 __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
 {
     constexpr int F = 32 / L;
+    constexpr bool CH_SMEM = L >= 16;
+    constexpr uint32_t FULL = 0xffffffffu;
     extern __shared__ __align__(16) uint32_t smw[];
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    uint32_t *wbase = smw + (size_t)wib * a.warp_words;
-    float *llr = reinterpret_cast<float *>(wbase);
-    uint32_t *ps = wbase + 32 * a.ss;
-    uint32_t *uh = ps + 32 * a.psw;
-
-    const int n = a.code.n, N = a.code.N, tp = a.tp;
-    const int grp = lane / L, gbase = grp * L, pl = lane - gbase;
-    const uint32_t gmask_lo = (L == 32) ? 0xffffffffu : ((1u << L) - 1u);
-    const int total = a.count != nullptr ? *a.count : a.B;
+    const int N = a.code.N, n = a.code.n, tp = a.tp, ss = a.ss, psw = a.psw, uhs = a.uhs;
     const int NW = (N + 31) >> 5;
+    uint32_t *frz = smw;      // CTA-shared frozen mask
+    uint32_t *dam = smw + NW; // CTA-shared decision-aided mask
+    const int lane = threadIdx.x & 31;
+    uint32_t *wbase = smw + a.table_words + (size_t)(threadIdx.x >> 5) * a.warp_words;
+    float *llr = reinterpret_cast<float *>(wbase);
+    uint32_t *ps = wbase + 32 * ss;
+    uint32_t *uh = ps + 32 * psw;
+    float *cand = reinterpret_cast<float *>(uh + 32 * uhs);
+    float *chs = cand + 64;
+    for (int w = threadIdx.x; w < NW; w += blockDim.x) {
+        frz[w] = a.code.frozen_bits[w];
+        dam[w] = a.code.da_bits != nullptr ? a.code.da_bits[w] : 0u;
+    }
+    __syncthreads();
+
+    const int grp = lane / L, gbase = grp * L, pl = lane - gbase;
+    const uint32_t gmask_lo = (L == 32) ? FULL : ((1u << L) - 1u);
+    const int total = a.count != nullptr ? *a.count : a.B;
+    float *own = llr + lane * ss;
+    uint32_t *urow = uh + lane * uhs;
+    uint32_t *prow = ps + lane * psw;
+    float *cg = cand + grp * 2 * L;
 
     for (;;) {
         int base = 0;
         if (lane == 0)
             base = atomicAdd(a.work, F);
-        base = __shfl_sync(0xffffffffu, base, 0);
+        base = __shfl_sync(FULL, base, 0);
         if (base >= total)
             break;
         const int qi = base + grp;
         const bool grp_live = qi < total;
         const int frame = grp_live ? (a.queue != nullptr ? a.queue[qi] : qi) : 0;
-
-        Tree T;
-        T.ch = a.llr + (size_t)frame * N;
-        T.ps = ps;
-        T.n = n;
-        T.psw = a.psw;
-        T.pl = 0;
-        T.pp = 0;
-        for (int s = 0; s < 12; ++s) {
-            T.pl = set_slot(T.pl, s, lane);
-            T.pp = set_slot(T.pp, s, lane);
+        const float *ch;
+        if (CH_SMEM) {
+            float *mine = chs + grp * N;
+            const float *g = a.llr + (size_t)frame * N;
+            for (int t = 4 * pl; t < N; t += 4 * L)
+                *reinterpret_cast<float4 *>(mine + t) = __ldg(reinterpret_cast<const float4 *>(g + t));
+            ch = mine;
+            __syncwarp();
+        } else {
+            ch = a.llr + (size_t)frame * N;
         }
+
+        uint64_t lanepat = 0; // the lane index in every 5-bit pointer field
+        for (int s = 0; s < 12; ++s)
+            lanepat = set_slot(lanepat, s, lane);
+        uint64_t pll = lanepat, ppp = lanepat; // slot pointers: LLR levels, partial-sum levels
         int P = grp_live ? 1 : 0;
         float metric = 0.0f;
-        float *own = llr + lane * a.ss;
 
         for (int i = 0; i < N; ++i) {
-            T.i = i;
             const bool act = pl < P;
             // ---- descent: levels min(start, tp) .. 0 ----
+            float lam = 0.0f;
             if (act) {
                 const int start = (i == 0) ? n - 1 : __ffs(i) - 1;
-                for (int s = start < tp ? start : tp; s >= 0; --s) {
-                    const int w = 1 << s;
-                    const bool gop = (i >> s) & 1;
-                    float *dst = own + w;
-                    if (s + 1 <= tp) {
-                        const float *src = llr + slot_of(T.pl, s + 1) * a.ss + 2 * w;
-                        const uint32_t *pw = ps + slot_of(T.pp, s) * a.psw + ps_off(s);
-                        if (w >= 4) {
-                            for (int t = 0; t < w; t += 4) {
-                                const float4 A = *reinterpret_cast<const float4 *>(src + t);
-                                const float4 B = *reinterpret_cast<const float4 *>(src + w + t);
-                                float4 o;
-                                if (gop) {
-                                    const uint32_t bits = pw[t >> 5] >> (t & 31);
-                                    o.x = scl_g(A.x, B.x, bits & 1u);
-                                    o.y = scl_g(A.y, B.y, (bits >> 1) & 1u);
-                                    o.z = scl_g(A.z, B.z, (bits >> 2) & 1u);
-                                    o.w = scl_g(A.w, B.w, (bits >> 3) & 1u);
-                                } else {
-                                    o.x = scl_f<FEX>(A.x, B.x);
-                                    o.y = scl_f<FEX>(A.y, B.y);
-                                    o.z = scl_f<FEX>(A.z, B.z);
-                                    o.w = scl_f<FEX>(A.w, B.w);
-                                }
-                                *reinterpret_cast<float4 *>(dst + t) = o;
-                            }
-                        } else {
-                            for (int t = 0; t < w; ++t) {
-                                const float A = src[t], B = src[w + t];
-                                dst[t] = gop ? scl_g(A, B, (pw[0] >> t) & 1u) : scl_f<FEX>(A, B);
-                            }
-                        }
-                    } else if (s + 1 == n) {
-                        // level n-1 straight from the channel (no virtual levels)
-                        const uint32_t *pw = ps + slot_of(T.pp, s) * a.psw + ps_off(s);
-                        for (int t = 0; t < w; ++t) {
-                            const float A = __ldg(T.ch + t), B = __ldg(T.ch + w + t);
-                            dst[t] = gop ? scl_g(A, B, (pw[t >> 5] >> (t & 31)) & 1u) : scl_f<FEX>(A, B);
-                        }
+                const int s0 = start < tp ? start : tp;
+                const int w0 = 1 << s0;
+                const uint32_t g0 = (i >> s0) & 1;
+                float *dst = own + w0;
+                const uint32_t *pw0 = ps + slot_of(ppp, s0) * psw + ps_off(s0);
+                int top = s0; // highest level written to the own slot, -1 once lam is known
+                if (s0 + 1 <= tp) {
+                    // the only level read through a slot pointer; everything below is own
+                    const float *src = llr + slot_of(pll, s0 + 1) * ss + 2 * w0;
+                    if (s0 >= 3) {
+                        if (g0)
+                            level_from<FEX, true>(dst, src, w0, pw0);
+                        else
+                            level_from<FEX, false>(dst, src, w0, pw0);
                     } else {
-                        const uint32_t *pw = ps + slot_of(T.pp, s) * a.psw + ps_off(s);
-                        for (int t = 0; t < w; ++t) {
-                            float A = 0.0f, B = 0.0f;
-                            if constexpr (NV > 0) {
-                                A = T.virt<NV, FEX>(t);
-                                B = T.virt<NV, FEX>(t + w);
-                            }
-                            dst[t] = gop ? scl_g(A, B, (pw[t >> 5] >> (t & 31)) & 1u) : scl_f<FEX>(A, B);
+                        lam = tail_from<FEX>(own, src, s0, g0, g0 ? pw0[0] : 0u);
+                        top = -1;
+                    }
+                } else if (NV == 0) {
+                    // level n-1 straight from the channel
+                    if (w0 >= 4) {
+                        if (g0)
+                            level_from<FEX, true>(dst, ch, w0, pw0);
+                        else
+                            level_from<FEX, false>(dst, ch, w0, pw0);
+                    } else {
+                        for (int t = 0; t < w0; ++t)
+                            dst[t] = g0 ? scl_g(ch[t], ch[w0 + t], bitw(pw0, t)) : scl_f<FEX>(ch[t], ch[w0 + t]);
+                    }
+                } else if (w0 >= 4) {
+                    if constexpr (NV > 0) {
+                        const uint32_t *psp[NV];
+                        uint32_t gm = 0;
+#pragma unroll
+                        for (int d = 0; d < NV; ++d) {
+                            const int r = n - NV + d;
+                            psp[d] = ps + slot_of(ppp, r) * psw + ps_off(r);
+                            gm |= ((uint32_t)(i >> r) & 1u) << d;
+                        }
+                        for (int t = 0; t < w0; t += 4) {
+                            const float4 A = virt_top4<NV, FEX>(ch, n, t, psp, gm);
+                            const float4 B = virt_top4<NV, FEX>(ch, n, t + w0, psp, gm);
+                            *reinterpret_cast<float4 *>(dst + t) = g0 ? g4(A, B, pw0[t >> 5] >> (t & 31)) : f4(A, B, FEX);
                         }
                     }
-                    T.pl = set_slot(T.pl, s, lane);
+                } else {
+                    if constexpr (NV > 0) {
+                        const uint32_t *psp[NV];
+                        uint32_t gm = 0;
+#pragma unroll
+                        for (int d = 0; d < NV; ++d) {
+                            const int r = n - NV + d;
+                            psp[d] = ps + slot_of(ppp, r) * psw + ps_off(r);
+                            gm |= ((uint32_t)(i >> r) & 1u) << d;
+                        }
+                        for (int t = 0; t < w0; ++t) {
+                            const float A = virt_top<NV, FEX>(ch, n, t, psp, gm);
+                            const float B = virt_top<NV, FEX>(ch, n, t + w0, psp, gm);
+                            dst[t] = g0 ? scl_g(A, B, bitw(pw0, t)) : scl_f<FEX>(A, B);
+                        }
+                    }
                 }
+                if (top >= 3) {
+                    for (int s = top - 1; s >= 3; --s)
+                        level_from<FEX, false>(own + (1 << s), own + (2 << s), 1 << s, nullptr);
+                    lam = tail_from<FEX>(own, own + 8, 2, 0u, 0u);
+                } else if (top >= 0) { // first level came from the channel / virtual levels of a tiny code
+                    for (int s = top - 1; s >= 0; --s)
+                        level_from<FEX, false>(own + (1 << s), own + (2 << s), 1 << s, nullptr);
+                    lam = own[1];
+                }
+                const uint64_t low = (5 * (s0 + 1) >= 64) ? ~0ull : ((1ull << (5 * (s0 + 1))) - 1ull);
+                pll = (pll & ~low) | (lanepat & low); // levels 0..s0 now live in the own slot
             }
             __syncwarp();
-            const float lam = act ? own[1] : 0.0f;
-            const bool frz = bit_of(a.code.frozen_bits, i);
-            const bool da = !frz && a.code.da_bits != nullptr && bit_of(a.code.da_bits, i);
+            const uint32_t fz = (frz[i >> 5] >> (i & 31)) & 1u;
+            const uint32_t dz = (dam[i >> 5] >> (i & 31)) & 1u;
+            float inc0, inc1;
+            metric_incs(lam, a.metric_exact, inc0, inc1);
             uint32_t u = 0;
-            bool newact = act;
-            if (frz || da) {
-                float inc0, inc1;
-                metric_incs(lam, a.metric_exact, inc0, inc1);
-                u = (da && lam < 0.0f) ? 1u : 0u;
+            int src = lane;
+            if (fz | dz) {
+                u = (dz && lam < 0.0f) ? 1u : 0u;
                 if (act)
                     metric += u ? inc1 : inc0;
             } else {
-                // ---- branch: 2L candidates, keep the L best by (metric, index) ----
-                float inc0, inc1;
-                metric_incs(lam, a.metric_exact, inc0, inc1);
+                // ---- branch: 2L candidates, keep the L best by (metric, candidate index) ----
                 const float c0 = act ? metric + inc0 : INFINITY;
                 const float c1 = act ? metric + inc1 : INFINITY;
-                bool k0 = act, k1 = act;
-                if (__any_sync(0xffffffffu, 2 * P > L)) {
-                    int r0 = 0, r1 = 0;
+                float gmax = fminf(c0, c1), bmin = fmaxf(c0, c1);
 #pragma unroll
-                    for (int q = 0; q < L; ++q) {
-                        const float v0 = __shfl_sync(0xffffffffu, c0, gbase + q);
-                        const float v1 = __shfl_sync(0xffffffffu, c1, gbase + q);
-                        r0 += (v0 < c0 || (v0 == c0 && q <= pl)) + (v1 < c0);
-                        r1 += (v0 <= c1) + (v1 < c1 || (v1 == c1 && q <= pl));
-                    }
-                    k0 = act && r0 <= L && c0 < INFINITY;
-                    k1 = act && r1 <= L && c1 < INFINITY;
+                for (int off = 1; off < L; off <<= 1) {
+                    gmax = fmaxf(gmax, __shfl_xor_sync(FULL, gmax, off));
+                    bmin = fminf(bmin, __shfl_xor_sync(FULL, bmin, off));
                 }
-                const uint32_t freeM = (__ballot_sync(0xffffffffu, act && !k0 && !k1) >> gbase) & gmask_lo;
-                const uint32_t dupM = (__ballot_sync(0xffffffffu, act && k0 && k1) >> gbase) & gmask_lo;
-                const int nf = __popc(freeM), nd = __popc(dupM);
-                const bool surv = act && (k0 || k1);
-                int src = lane;
-                if (surv) {
-                    u = k0 ? 0u : 1u;
-                    metric = k0 ? c0 : c1;
+                if (__all_sync(FULL, !grp_live || (P == L && gmax < bmin))) {
+                    // every agreeing child beats every disagreeing child: the survivors
+                    // are the agreeing children, no slot moves, no clones
+                    const bool z = c0 < c1;
+                    u = z ? 0u : 1u;
+                    if (act)
+                        metric = z ? c0 : c1;
                 } else {
-                    const int r = act ? __popc(freeM & ((1u << pl) - 1u)) : nf + (pl - P);
-                    if (pl < L && r < nd) {
-                        // r-th set bit of dupM = the parent this slot clones
-                        uint32_t m = dupM;
-                        for (int z = 0; z < r; ++z)
-                            m &= m - 1u;
-                        src = gbase + __ffs(m) - 1;
+                    bool k0 = act, k1 = act;
+                    if (__any_sync(FULL, 2 * P > L)) {
+                        cg[pl] = c0;
+                        cg[L + pl] = c1;
+                        __syncwarp();
+                        int lt0 = 0, lt1 = 0;
+#pragma unroll
+                        for (int j = 0; j < 2 * L; j += 4) {
+                            const float4 v = *reinterpret_cast<const float4 *>(cg + j);
+                            lt0 += (v.x < c0) + (v.y < c0) + (v.z < c0) + (v.w < c0);
+                            lt1 += (v.x < c1) + (v.y < c1) + (v.z < c1) + (v.w < c1);
+                        }
+                        // no ties among the 2P finite candidates <=> their strict ranks sum to fc(fc-1)/2
+                        int sum = (act ? lt0 + lt1 : 0);
+#pragma unroll
+                        for (int off = 1; off < L; off <<= 1)
+                            sum += __shfl_xor_sync(FULL, sum, off);
+                        const bool tie = sum != P * (2 * P - 1);
+                        if (__any_sync(FULL, tie)) {
+                            lt0 = 0;
+                            lt1 = 0;
+                            for (int j = 0; j < 2 * L; ++j) {
+                                const float v = cg[j];
+                                lt0 += (v < c0) || (v == c0 && j < pl);
+                                lt1 += (v < c1) || (v == c1 && j < L + pl);
+                            }
+                        }
+                        k0 = act && lt0 < L;
+                        k1 = act && lt1 < L;
+                        __syncwarp();
                     }
+                    const uint32_t freeM = (__ballot_sync(FULL, act && !k0 && !k1) >> gbase) & gmask_lo;
+                    const uint32_t dupM = (__ballot_sync(FULL, act && k0 && k1) >> gbase) & gmask_lo;
+                    const int nf = __popc(freeM), nd = __popc(dupM);
+                    const bool surv = act && (k0 || k1);
+                    if (surv) {
+                        u = k0 ? 0u : 1u;
+                        metric = k0 ? c0 : c1;
+                    } else {
+                        const int r = act ? __popc(freeM & ((1u << pl) - 1u)) : nf + (pl - P);
+                        if (r < nd) {
+                            uint32_t m = dupM; // the r-th set bit of dupM is the parent this slot clones
+                            for (int z = 0; z < r; ++z)
+                                m &= m - 1u;
+                            src = gbase + __ffs(m) - 1;
+                        }
+                    }
+                    const float pc1 = __shfl_sync(FULL, c1, src);
+                    const uint32_t pl_lo = __shfl_sync(FULL, (uint32_t)pll, src);
+                    const uint32_t pl_hi = __shfl_sync(FULL, (uint32_t)(pll >> 32), src);
+                    const uint32_t pp_lo = __shfl_sync(FULL, (uint32_t)ppp, src);
+                    const uint32_t pp_hi = __shfl_sync(FULL, (uint32_t)(ppp >> 32), src);
+                    if (src != lane) {
+                        u = 1u;
+                        metric = pc1;
+                        pll = ((uint64_t)pl_hi << 32) | pl_lo;
+                        ppp = ((uint64_t)pp_hi << 32) | pp_lo;
+                        const uint32_t *from = uh + src * uhs;
+                        for (int w = 0; w <= (i >> 5); ++w)
+                            urow[w] = from[w];
+                    }
+                    P = P == 0 ? 0 : P - nf + nd;
+                    __syncwarp();
                 }
-                const bool clone = src != lane;
-                const float pc1 = __shfl_sync(0xffffffffu, c1, src);
-                const uint32_t pl_lo = __shfl_sync(0xffffffffu, (uint32_t)T.pl, src);
-                const uint32_t pl_hi = __shfl_sync(0xffffffffu, (uint32_t)(T.pl >> 32), src);
-                const uint32_t pp_lo = __shfl_sync(0xffffffffu, (uint32_t)T.pp, src);
-                const uint32_t pp_hi = __shfl_sync(0xffffffffu, (uint32_t)(T.pp >> 32), src);
-                if (clone) {
-                    u = 1u;
-                    metric = pc1;
-                    T.pl = ((uint64_t)pl_hi << 32) | pl_lo;
-                    T.pp = ((uint64_t)pp_hi << 32) | pp_lo;
-                    const uint32_t *from = uh + src * a.uhs;
-                    uint32_t *to = uh + lane * a.uhs;
-                    for (int w = 0; w <= (i >> 5); ++w)
-                        to[w] = from[w];
-                }
-                newact = surv || clone;
-                P = P == 0 ? 0 : P - nf + nd;
-                __syncwarp();
             }
-            if (newact) {
+            if (pl < P) {
                 // record the decision, then fold it into the partial sums
-                uint32_t *row = uh + lane * a.uhs;
                 const uint32_t bm = 1u << (i & 31);
-                row[i >> 5] = u ? (row[i >> 5] | bm) : (row[i >> 5] & ~bm);
-                int S = __ffs(~i) - 1; // trailing ones of i
+                urow[i >> 5] = u ? (urow[i >> 5] | bm) : (urow[i >> 5] & ~bm);
+                const int S = __ffs(~i) - 1; // trailing ones of i
                 if (S < n) {
-                    uint32_t F5 = u ? 1u : 0u;
+                    uint32_t F5 = u;
                     const int lo = S < 5 ? S : 5;
                     for (int s = 0; s < lo; ++s) {
                         const int len = 1 << s;
-                        const uint32_t pv = ps[slot_of(T.pp, s) * a.psw + ps_off(s)];
-                        const uint32_t msk = (len == 32) ? 0xffffffffu : ((1u << len) - 1u);
-                        F5 = ((pv ^ F5) & msk) | (F5 << len);
+                        const uint32_t pv = ps[slot_of(ppp, s) * psw + s];
+                        F5 = ((pv ^ F5) & ((1u << len) - 1u)) | (F5 << len);
                     }
-                    uint32_t *dst = ps + lane * a.psw + ps_off(S);
+                    uint32_t *dst = prow + ps_off(S);
                     if (S <= 5) {
                         dst[0] = F5;
                     } else {
@@ -325,11 +508,11 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
                             uint32_t v = F5;
                             for (int s = 5; s < S; ++s)
                                 if (((w >> (s - 5)) & 1) == 0)
-                                    v ^= ps[slot_of(T.pp, s) * a.psw + ps_off(s) + (w & ((1 << (s - 5)) - 1))];
+                                    v ^= ps[slot_of(ppp, s) * psw + ps_off(s) + (w & ((1 << (s - 5)) - 1))];
                             dst[w] = v;
                         }
                     }
-                    T.pp = set_slot(T.pp, S, lane);
+                    ppp = set_slot(ppp, S, lane);
                 }
             }
             __syncwarp();
@@ -340,9 +523,8 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
         bool ok = false;
         if (act && a.code.crc_width > 0) {
             uint32_t syn = 0;
-            const uint32_t *row = uh + lane * a.uhs;
             for (int w = 0; w < NW; ++w) {
-                uint32_t v = row[w];
+                uint32_t v = urow[w];
                 if (32 * w + 32 > N)
                     v &= (1u << (N & 31)) - 1u;
                 while (v) {
@@ -353,21 +535,21 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
             }
             ok = syn == a.code.crc_offset;
         }
-        const uint32_t okM = (__ballot_sync(0xffffffffu, ok) >> gbase) & gmask_lo;
-        const bool cand = okM ? ok : act;
-        float key = cand ? metric : INFINITY;
-        int who = cand ? pl : L;
+        const uint32_t okM = (__ballot_sync(FULL, ok) >> gbase) & gmask_lo;
+        const bool cnd = okM ? ok : act;
+        float key = cnd ? metric : INFINITY;
+        int who = cnd ? pl : L;
 #pragma unroll
         for (int off = 1; off < L; off <<= 1) {
-            const float k2 = __shfl_xor_sync(0xffffffffu, key, off);
-            const int w2 = __shfl_xor_sync(0xffffffffu, who, off);
+            const float k2 = __shfl_xor_sync(FULL, key, off);
+            const int w2 = __shfl_xor_sync(FULL, who, off);
             if (k2 < key || (k2 == key && w2 < who)) {
                 key = k2;
                 who = w2;
             }
         }
         if (grp_live) {
-            const uint32_t *row = uh + (gbase + who) * a.uhs;
+            const uint32_t *row = uh + (gbase + who) * uhs;
             if (a.u_bits != nullptr)
                 for (int w = pl; w < NW; w += L) {
                     uint32_t v = row[w];
@@ -380,7 +562,7 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
                 for (int w = pl; w < MW; w += L) {
                     uint32_t v = 0;
                     for (int b = 0; b < 32 && 32 * w + b < a.code.m; ++b)
-                        v |= bit_of(row, __ldg(a.code.info_pos + 32 * w + b)) << b;
+                        v |= bitw(row, __ldg(a.code.info_pos + 32 * w + b)) << b;
                     a.payload[(size_t)frame * MW + w] = v;
                 }
             }
@@ -401,15 +583,14 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
 
 // ------------------------------------------------------------- launchers --
 
-
 int scl_prepare(SclArgs &a, int nv_req)
 {
     const int n = a.code.n;
     int nv = nv_req;
     if (nv < 0)
         nv = 0;
-    if (nv > n - 1)
-        nv = n - 1;
+    if (nv > n - 2)
+        nv = n - 2 > 0 ? n - 2 : 0; // keep at least levels 0..1 stored (float4 needs tp >= 2 anyway)
     if (nv > 3)
         nv = 3;
     a.nv = nv;
@@ -418,21 +599,26 @@ int scl_prepare(SclArgs &a, int nv_req)
     a.psw = ps_off(n) | 1; // words for levels 0..n-1, odd stride
     const int nw = (a.code.N + 31) >> 5;
     a.uhs = nw | 1;
-    a.warp_words = 32 * (a.ss + a.psw + a.uhs);
+    a.table_words = (2 * nw + 3) & ~3;
     return PC_OK;
 }
 
 template <int L, bool FEX, int NV>
-static int launch_scl_t(const SclArgs &a, int wpc, int max_warps, cudaStream_t s)
+static int launch_scl_t(SclArgs a, int wpc, int max_warps, cudaStream_t s)
 {
     auto kern = k_scl<L, FEX, NV>;
+    constexpr int F = 32 / L;
+    const int ch_words = (L >= 16) ? F * a.code.N : 0;
+    a.warp_words = 32 * (a.ss + a.psw + a.uhs) + 64 + ch_words;
+    a.warp_words = (a.warp_words + 3) & ~3;
     const size_t per_warp = (size_t)a.warp_words * 4;
+    const size_t table = (size_t)a.table_words * 4;
     const size_t smem_cap = 227 * 1024;
-    if (per_warp > smem_cap)
+    if (table + per_warp > smem_cap)
         return PC_ERR_UNSUPPORTED;
-    while (wpc > 1 && (size_t)wpc * per_warp > smem_cap)
+    while (wpc > 1 && table + (size_t)wpc * per_warp > smem_cap)
         --wpc;
-    const size_t smem = (size_t)wpc * per_warp;
+    const size_t smem = table + (size_t)wpc * per_warp;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return PC_ERR_CUDA;
     int dev = 0, sms = 0, per_sm = 0;
