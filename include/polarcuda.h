@@ -62,10 +62,14 @@ typedef struct pc_code {
 } pc_code_t;
 
 /* BpConfig, bp.py:40-57.  g_mode 0 = exact, 1 = min; stop_mode 0 = crc,
- * 1 = reencode, 2 = none.  threads_per_frame 0 = library default. */
+ * 1 = reencode, 2 = none.  threads_per_frame 0 = library default.
+ * kernel: 0 = auto (register/shuffle kernel when eligible), 1 = shared-memory
+ * kernel, 2 = register/shuffle kernel (N = 128..2048, crc/none stop, no soft_x);
+ * a performance knob that does not change results. */
 typedef struct pc_bp_cfg {
     int32_t i_max, g_mode, stop_mode, threads_per_frame;
     float llr_max;
+    int32_t kernel;
 } pc_bp_cfg_t;
 
 /* SclConfig, scl.py:39-66.  L in {1,2,4,8,16,32}.  virtual_levels: how many of

@@ -60,6 +60,7 @@ class PcBpCfg(C.Structure):
         ("stop_mode", C.c_int32),
         ("threads_per_frame", C.c_int32),
         ("llr_max", C.c_float),
+        ("kernel", C.c_int32),
     ]
 
 

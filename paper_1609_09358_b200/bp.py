@@ -65,13 +65,14 @@ class BpConfig:
         if self.stop_mode not in _STOP_MODES:
             raise ValueError(f"unknown stop mode {self.stop_mode!r}")
 
-    def native(self, threads_per_frame: int = 0) -> nat.PcBpCfg:
+    def native(self, threads_per_frame: int = 0, kernel: int | None = None) -> nat.PcBpCfg:
         return nat.PcBpCfg(
             self.i_max,
             _G_MODES.index(self.g_mode),
             _STOP_MODES.index(self.stop_mode),
             threads_per_frame or nat.env_int("PC_BP_TPF", 0),
             float(self.llr_max),
+            nat.env_int("PC_BP_KERNEL", 0) if kernel is None else kernel,
         )
 
 

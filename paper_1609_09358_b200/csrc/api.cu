@@ -78,7 +78,7 @@ int pc_bp_decode(const float *llr, int32_t B, const pc_code_t *code, const pc_bp
     a.iters = iters;
     a.conv = converged;
     a.t_done = t_done;
-    return launch_bp_decode(a, cfg->g_mode, cfg->threads_per_frame, (cudaStream_t)stream);
+    return launch_bp_decode(a, cfg->g_mode, cfg->threads_per_frame, cfg->kernel, (cudaStream_t)stream);
 }
 
 int pc_bp_iterate(float *l_msgs, float *r_msgs, int32_t B, const pc_code_t *code, const pc_bp_cfg_t *cfg,

@@ -21,31 +21,10 @@
 // which equals logaddexp(0,a+b) - logaddexp(a,b) of bp.py:95 (4 MUFU ops).
 // The magnitude is clamped to [0, m], the range the exact value lies in.
 #include "args.cuh"
+#include "bp_math.cuh"
 
 namespace pc {
 
-
-__device__ __forceinline__ float sp_neg(float x) // log1p(exp(-x)), x >= 0
-{
-    return PC_LN2 * lg2_approx(1.0f + ex2_approx(-x * PC_LOG2E));
-}
-
-template <int GMODE>
-__device__ __forceinline__ float bp_g(float a, float b, float lim)
-{
-    const float aa = fabsf(a), ab = fabsf(b);
-    const float m = fminf(aa, ab);
-    float mag;
-    if (GMODE == 0) {
-        mag = m + sp_neg(aa + ab) - sp_neg(fabsf(aa - ab));
-        mag = fminf(fmaxf(mag, 0.0f), m);
-    } else {
-        mag = (a == 0.0f || b == 0.0f) ? 0.0f : m;
-    }
-    mag = fminf(mag, lim);
-    const uint32_t sgn = (__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u;
-    return __uint_as_float(__float_as_uint(mag) ^ sgn);
-}
 
 // One boundary of the R sweep (writes R[j]) or L sweep (writes L[j-1]).
 // Rprev = R[j-1] (nullptr for j == 1: use the frozen prior), Lj = L[j].
@@ -365,10 +344,14 @@ static int launch_bp_g(const BpArgs &a, int logn, int tpf, cudaStream_t s)
     }
 }
 
-int launch_bp_decode(const BpArgs &a, int g_mode, int tpf, cudaStream_t s)
+int launch_bp_decode(const BpArgs &a, int g_mode, int tpf, int kernel, cudaStream_t s)
 {
     if (a.B == 0)
         return PC_OK;
+    if (kernel == 2 && !bp2_eligible(a, tpf))
+        return PC_ERR_UNSUPPORTED;
+    if (kernel != 1 && bp2_eligible(a, tpf))
+        return launch_bp2(a, g_mode, tpf, s);
     return g_mode == 0 ? launch_bp_g<0>(a, a.code.n, tpf, s) : launch_bp_g<1>(a, a.code.n, tpf, s);
 }
 

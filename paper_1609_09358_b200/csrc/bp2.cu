@@ -1,0 +1,343 @@
+// bp2.cu -- K1 v2: BP decoding with register-resident low stages and
+// warp-shuffle butterflies (sm_100a).  Same arithmetic and stop cadence as
+// k_bp_decode (bp.cu), which restates bp.py:120-217.
+//
+// Node ownership: thread t of the frame owns the Q = N / TPF consecutive nodes
+// base(t) .. base(t)+Q-1 with base(t) = warp*32Q + lane*Q.  Then
+//   * boundaries 1..B (B = log2 Q) join nodes inside one thread: register
+//     butterflies, no communication at all;
+//   * boundaries B+1..B+5 join nodes of lanes lane ^ 2^(j-1-B) of the same
+//     warp: each lane exchanges (R[j-1], L[j]) of its nodes with one shuffle
+//     pair and computes the node update of its own half of the element
+//     (i1 lanes:  g(a, l2 + r2) / g(l1, l2 + r2); i2 lanes: g(a, l1) + r2 /
+//     g(a, l1) + l2, clipped);
+//   * only boundaries above BW = B+5 go through shared memory, one CTA barrier
+//     each.
+// The message stages 1..BW-1 of a thread's nodes therefore live in registers
+// across iterations (the same thread owns the same nodes in both sweeps), and
+// shared memory holds only R[BW..n-1] and L[BW..n].  At N=1024, TPF=256 that is
+// 7 rows (28 KB) instead of 19, and 7 CTA barriers per iteration instead of 20.
+#include "args.cuh"
+#include "bp_math.cuh"
+
+namespace pc {
+
+template <int V>
+struct ilog2 {
+    static constexpr int value = 1 + ilog2<V / 2>::value;
+};
+template <>
+struct ilog2<1> {
+    static constexpr int value = 0;
+};
+
+template <int LOGN, int TPF, int GMODE>
+__global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
+{
+    constexpr int N = 1 << LOGN;
+    constexpr int Q = N / TPF;
+    constexpr int B = ilog2<Q>::value;
+    constexpr int BW = B + 5;        // last warp-local boundary (TPF >= 32 => BW <= LOGN)
+    constexpr int NSR = LOGN - BW;   // shared R rows: stages BW..LOGN-1
+    constexpr int NSL = LOGN - BW + 1; // shared L rows: stages BW..LOGN
+    constexpr int NREG = BW - 1;     // register stages 1..BW-1
+    constexpr int NW = (N + 31) / 32;
+    constexpr int NWARP = TPF / 32;
+    constexpr int PPT = N / 2 / TPF; // shared-memory boundary elements per thread
+    static_assert(TPF >= 32 && Q >= 2 && Q <= 32 && BW <= LOGN, "bp2 geometry");
+
+    extern __shared__ __align__(16) float sm[];
+    float *Rs = sm;           // R[BW + r], r < NSR
+    float *Ls = sm + NSR * N; // L[BW + r], r < NSL
+    uint8_t *ub = reinterpret_cast<uint8_t *>(Ls + NSL * N);
+    __shared__ uint32_t frz[NW];
+    __shared__ uint32_t red[NWARP];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int f = blockIdx.x;
+    const float lim = a.llr_max;
+    const int base = warp * 32 * Q + lane * Q;
+
+    for (int w = tid; w < NW; w += TPF)
+        frz[w] = a.code.frozen_bits[w];
+    const float *x = a.llr + (size_t)f * N;
+    float *Lch = Ls + (NSL - 1) * N;
+    for (int i = 4 * tid; i < N; i += 4 * TPF) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(x + i));
+        *reinterpret_cast<float4 *>(Lch + i) = make_float4(clampf(v.x, lim), clampf(v.y, lim), clampf(v.z, lim),
+                                                          clampf(v.w, lim));
+    }
+    for (int i = tid; i < NSR * N; i += TPF)
+        Rs[i] = 0.0f;
+    for (int i = tid; i < (NSL - 1) * N; i += TPF)
+        Ls[i] = 0.0f;
+    float Rr[NREG][Q], Lr[NREG][Q];
+#pragma unroll
+    for (int s = 0; s < NREG; ++s)
+#pragma unroll
+        for (int r = 0; r < Q; ++r)
+            Rr[s][r] = Lr[s][r] = 0.0f;
+    uint32_t col[Q];
+#pragma unroll
+    for (int r = 0; r < Q; ++r)
+        col[r] = a.stop_mode == 0 ? __ldg(a.code.crc_cols + base + r) : 0u;
+    __syncthreads();
+    const uint32_t fw = frz[base >> 5] >> (base & 31);
+    float pri[Q];
+#pragma unroll
+    for (int r = 0; r < Q; ++r)
+        pri[r] = ((fw >> r) & 1u) ? lim : 0.0f;
+
+    // compile-time stage accessors (every loop below is fully unrolled, so the
+    // register arrays are indexed with constants)
+#define RGET(s, r) ((s) == 0 ? pri[r] : ((s) <= NREG ? Rr[(s) > 0 ? (s) - 1 : 0][r] : Rs[((s) - BW) * N + base + (r)]))
+#define LGET(s, r) ((s) <= NREG ? Lr[(s) > 0 ? (s) - 1 : 0][r] : Ls[((s) - BW) * N + base + (r)])
+
+    float su[Q];
+    int it = 0;
+    bool stop = false;
+    for (;;) {
+        ++it;
+        // ================= R sweep =================
+#pragma unroll
+        for (int j = 1; j <= B; ++j) { // inside the thread
+            const int h = 1 << (j - 1);
+#pragma unroll
+            for (int r1 = 0; r1 < Q; ++r1) {
+                if (r1 & h)
+                    continue;
+                const int r2 = r1 + h;
+                const float av = RGET(j - 1, r1), r2v = RGET(j - 1, r2), l1 = LGET(j, r1), l2 = LGET(j, r2);
+                Rr[j - 1][r1] = bp_g<GMODE>(av, l2 + r2v, lim);
+                Rr[j - 1][r2] = clampf(bp_g<GMODE>(av, l1, lim) + r2v, lim);
+            }
+        }
+#pragma unroll
+        for (int j = B + 1; j <= BW; ++j) { // across lanes of the warp
+            if (j == LOGN)
+                break; // R[n] is not read by the sweeps
+            const int msk = 1 << (j - 1 - B);
+            const bool hi = lane & msk;
+#pragma unroll
+            for (int r = 0; r < Q; ++r) {
+                const float myR = RGET(j - 1, r), myL = LGET(j, r);
+                const float xo = __shfl_xor_sync(0xffffffffu, myR, msk);
+                const float yo = __shfl_xor_sync(0xffffffffu, myL, msk);
+                // i1 lane: g(a, l2 + r2) = g(myR, yo + xo); i2 lane: g(a, l1) + r2 = g(xo, yo) + myR
+                float o = bp_g<GMODE>(hi ? xo : myR, hi ? yo : yo + xo, lim);
+                if (hi)
+                    o = clampf(o + myR, lim);
+                if (j <= NREG)
+                    Rr[j - 1][r] = o;
+                else
+                    Rs[(j - BW) * N + base + r] = o;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = BW + 1; j <= LOGN - 1; ++j) { // shared-memory boundaries
+            const int h = 1 << (j - 1);
+            const float *Rp = Rs + (j - 1 - BW) * N;
+            float *Rd = Rs + (j - BW) * N;
+            const float *Lj = Ls + (j - BW) * N;
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+                const int p = tid + q * TPF;
+                const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
+                const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
+                Rd[i1] = bp_g<GMODE>(av, l2 + r2v, lim);
+                Rd[i2] = clampf(bp_g<GMODE>(av, l1, lim) + r2v, lim);
+            }
+            __syncthreads();
+        }
+        // ================= L sweep =================
+#pragma unroll
+        for (int j = LOGN; j >= BW + 1; --j) {
+            const int h = 1 << (j - 1);
+            const float *Rp = Rs + (j - 1 - BW) * N;
+            const float *Lj = Ls + (j - BW) * N;
+            float *Ld = Ls + (j - 1 - BW) * N;
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+                const int p = tid + q * TPF;
+                const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
+                const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
+                Ld[i1] = bp_g<GMODE>(l1, l2 + r2v, lim);
+                Ld[i2] = clampf(bp_g<GMODE>(av, l1, lim) + l2, lim);
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int j = BW; j >= B + 1; --j) {
+            const int msk = 1 << (j - 1 - B);
+            const bool hi = lane & msk;
+#pragma unroll
+            for (int r = 0; r < Q; ++r) {
+                const float myR = RGET(j - 1, r), myL = LGET(j, r);
+                const float xo = __shfl_xor_sync(0xffffffffu, myR, msk);
+                const float yo = __shfl_xor_sync(0xffffffffu, myL, msk);
+                // i1 lane: g(l1, l2 + r2) = g(myL, yo + xo); i2 lane: g(a, l1) + l2 = g(xo, yo) + myL
+                float o = bp_g<GMODE>(hi ? xo : myL, hi ? yo : yo + xo, lim);
+                if (hi)
+                    o = clampf(o + myL, lim);
+                Lr[j - 2][r] = o; // j - 1 >= B >= 1 is a register stage
+            }
+        }
+#pragma unroll
+        for (int j = B; j >= 1; --j) {
+            const int h = 1 << (j - 1);
+#pragma unroll
+            for (int r1 = 0; r1 < Q; ++r1) {
+                if (r1 & h)
+                    continue;
+                const int r2 = r1 + h;
+                const float av = RGET(j - 1, r1), r2v = RGET(j - 1, r2), l1 = LGET(j, r1), l2 = LGET(j, r2);
+                const float o1 = bp_g<GMODE>(l1, l2 + r2v, lim);
+                const float o2 = clampf(bp_g<GMODE>(av, l1, lim) + l2, lim);
+                if (j > 1) {
+                    Lr[j - 2][r1] = o1;
+                    Lr[j - 2][r2] = o2;
+                } else {
+                    su[r1] = o1 + av; // soft_u = L[0] + R[0]
+                    su[r2] = o2 + r2v;
+                }
+            }
+        }
+        // ================= stop rule (crc or none) =================
+        if (a.stop_mode == 0) {
+            uint32_t syn = 0;
+#pragma unroll
+            for (int r = 0; r < Q; ++r)
+                syn ^= (su[r] < 0.0f) ? col[r] : 0u;
+            syn = __reduce_xor_sync(0xffffffffu, syn);
+            if (lane == 0)
+                red[warp] = syn;
+            __syncthreads();
+            uint32_t tot = 0;
+#pragma unroll
+            for (int w = 0; w < NWARP; ++w)
+                tot ^= red[w];
+            stop = (tot == a.code.crc_offset);
+        }
+        if (stop || it >= a.i_max)
+            break;
+    }
+
+    // ---- outputs ----
+    if (tid == 0) {
+        if (a.t_done != nullptr)
+            a.t_done[f] = globaltimer();
+        a.iters[f] = stop ? it : a.i_max;
+        a.conv[f] = stop ? 1 : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < Q; ++r)
+        ub[base + r] = su[r] < 0.0f;
+    if (a.soft_u != nullptr) {
+#pragma unroll
+        for (int r = 0; r < Q; r += 2)
+            *reinterpret_cast<float2 *>(a.soft_u + (size_t)f * N + base + r) = make_float2(su[r], su[r + 1]);
+    }
+    __syncthreads();
+    if (a.u_bits != nullptr)
+        for (int w = tid; w < NW; w += TPF) {
+            uint32_t v = 0;
+            for (int b = 0; b < 32; ++b)
+                v |= (uint32_t)ub[32 * w + b] << b;
+            a.u_bits[(size_t)f * NW + w] = v;
+        }
+    if (a.payload != nullptr) {
+        const int MW = (a.code.m + 31) >> 5;
+        for (int w = tid; w < MW; w += TPF) {
+            uint32_t v = 0;
+            for (int b = 0; b < 32 && 32 * w + b < a.code.m; ++b)
+                v |= (uint32_t)ub[__ldg(a.code.info_pos + 32 * w + b)] << b;
+            a.payload[(size_t)f * MW + w] = v;
+        }
+    }
+}
+
+#undef RGET
+#undef LGET
+
+static size_t bp2_smem_bytes(int logn, int tpf)
+{
+    const int N = 1 << logn;
+    int q = N / tpf, b = 0;
+    while ((1 << b) < q)
+        ++b;
+    const int bw = b + 5;
+    return (size_t)((logn - bw) + (logn - bw + 1)) * N * sizeof(float) + N;
+}
+
+template <int LOGN, int TPF, int GMODE>
+static int launch_bp2_t(const BpArgs &a, cudaStream_t s)
+{
+    auto kern = k_bp2<LOGN, TPF, GMODE>;
+    const size_t smem = bp2_smem_bytes(LOGN, TPF);
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return PC_ERR_CUDA;
+    kern<<<a.B, TPF, smem, s>>>(a);
+    return cudaGetLastError() == cudaSuccess ? PC_OK : PC_ERR_CUDA;
+}
+
+template <int LOGN, int GMODE>
+static int launch_bp2_n(const BpArgs &a, int tpf, cudaStream_t s)
+{
+    constexpr int N = 1 << LOGN;
+    constexpr int LO = N / 32 > 32 ? N / 32 : 32; // Q <= 32 nodes per thread
+    constexpr int HI = N / 2;                     // Q >= 2
+    if (tpf <= 0)
+        tpf = N / 4 >= 256 ? 256 : N / 4;
+    if (tpf < LO || tpf > HI)
+        return PC_ERR_UNSUPPORTED;
+#define PC_BP2_CASE(T)                                                                                                 \
+    case T: return launch_bp2_t<LOGN, (T < LO ? LO : (T > HI ? HI : T)), GMODE>(a, s);
+    switch (tpf) {
+        PC_BP2_CASE(32)
+        PC_BP2_CASE(64)
+        PC_BP2_CASE(128)
+        PC_BP2_CASE(256)
+        PC_BP2_CASE(512)
+        PC_BP2_CASE(1024)
+    default: return PC_ERR_UNSUPPORTED;
+    }
+#undef PC_BP2_CASE
+}
+
+// K1 v2 covers N = 128 .. 2048 with the crc / none stop rules and no soft_x.
+bool bp2_eligible(const BpArgs &a, int tpf)
+{
+    const int N = a.code.N;
+    const int lo = N / 32 > 32 ? N / 32 : 32;
+    return a.code.n >= 7 && a.code.n <= 11 && a.stop_mode != 1 && a.soft_x == nullptr &&
+           (tpf <= 0 || (tpf >= lo && tpf <= N / 2));
+}
+
+int launch_bp2(const BpArgs &a, int g_mode, int tpf, cudaStream_t s)
+{
+    if (a.B == 0)
+        return PC_OK;
+    const int n = a.code.n;
+    if (g_mode == 0) {
+        switch (n) {
+        case 7: return launch_bp2_n<7, 0>(a, tpf, s);
+        case 8: return launch_bp2_n<8, 0>(a, tpf, s);
+        case 9: return launch_bp2_n<9, 0>(a, tpf, s);
+        case 10: return launch_bp2_n<10, 0>(a, tpf, s);
+        case 11: return launch_bp2_n<11, 0>(a, tpf, s);
+        }
+    } else {
+        switch (n) {
+        case 7: return launch_bp2_n<7, 1>(a, tpf, s);
+        case 8: return launch_bp2_n<8, 1>(a, tpf, s);
+        case 9: return launch_bp2_n<9, 1>(a, tpf, s);
+        case 10: return launch_bp2_n<10, 1>(a, tpf, s);
+        case 11: return launch_bp2_n<11, 1>(a, tpf, s);
+        }
+    }
+    return PC_ERR_UNSUPPORTED;
+}
+
+} // namespace pc

@@ -155,8 +155,8 @@ def test_noiseless_converges_within_n_iterations():
         assert np.array_equal(got.u_hat[:, code.info_positions], msgs)
 
 
-@pytest.mark.parametrize("tpf", [64, 128, 256, 512])
-def test_threads_per_frame_variants_agree(tpf):
+@pytest.mark.parametrize("kernel,tpf", [(1, 64), (1, 128), (1, 256), (1, 512), (2, 128), (2, 256), (2, 512)])
+def test_kernel_variants_agree(kernel, tpf):
     code = CodeConfig(1024, 512, crc=16)
     sigma = ebno_to_sigma(2.5, code.rate)
     llrs = np.array([make_frame(code, sigma, frame_rng(9, 0, f))[1] for f in range(64)])
@@ -167,7 +167,7 @@ def test_threads_per_frame_variants_agree(tpf):
     base = bp_decode_batch(x, code, BpConfig(stop_mode="crc"))
     import ctypes
 
-    cfg = BpConfig(stop_mode="crc").native(threads_per_frame=tpf)
+    cfg = BpConfig(stop_mode="crc").native(threads_per_frame=tpf, kernel=kernel)
     dc = nat.device_code(code)
     u = torch.empty_like(base.u_hat)
     it = torch.empty_like(base.iterations_used)

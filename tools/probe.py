@@ -17,15 +17,15 @@ def ev(): return torch.cuda.Event(enable_timing=True)
 for eb in (1.0, 2.0, 3.0, 4.0):
     sigma = ebno_to_sigma(eb, code.rate)
     nat.check(lib.pc_gen_frames(1, 0, 0, B, sigma, dc.ref, msg.data_ptr(), llr.data_ptr(), st), 'gen')
-    for tpf in (128, 256, 512):
-        cfg = BpConfig(stop_mode='crc').native(threads_per_frame=tpf)
+    for kern, tpf in ((1, 256), (1, 512), (2, 128), (2, 256), (2, 512)):
+        cfg = BpConfig(stop_mode='crc').native(threads_per_frame=tpf, kernel=kern)
         for rep in range(2):
             a, b = ev(), ev(); a.record()
             nat.check(lib.pc_bp_decode(llr.data_ptr(), B, dc.ref, ctypes.byref(cfg), None, pay.data_ptr(), None, None, it.data_ptr(), cv.data_ptr(), None, st), 'bp')
             b.record(); torch.cuda.synchronize()
         ms = a.elapsed_time(b); iters = it.sum().item()
         gps = iters * 2 * 10 * 1024 / (ms * 1e-3)
-        print(f"BP eb={eb} tpf={tpf}: {ms:.2f} ms  mean_it={iters/B:.2f} gamma={(cv==0).float().mean().item():.3f} "
+        print(f"BP eb={eb} k={kern} tpf={tpf}: {ms:.2f} ms  mean_it={iters/B:.2f} gamma={(cv==0).float().mean().item():.3f} "
               f"g/s={gps:.3e} frac_xu(1.163e12)={gps/1.163e12:.3f} info Gbit/s={B*496/(ms*1e-3)/1e9:.3f}")
     cnt = torch.zeros((B,2), dtype=torch.int64, device='cuda')
 for L in (1, 4, 32):
