@@ -116,7 +116,7 @@ def run_reference(args):
     import oracle
 
     threads = oracle.cpu_count()
-    fpp = args.cpu_frames or max(128, 8 * threads)
+    fpp = args.cpu_frames or max(256, 24 * threads)
     vals = []
     for s in range(args.warmup + args.steps):
         v, busy = cpu_hybrid_sample(fpp if s >= args.warmup else max(8, threads), threads)
@@ -254,7 +254,7 @@ def run_gpu(args):
             traffic = None
     roofline = {
         "bound": "xu", "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
-        "traffic": traffic, "kernel": "k_bp_decode<10,512,0>",
+        "traffic": traffic, "kernel": "k_bp2<10,256,0> (register/shuffle BP, TPF=256)",
         "note": "exact-g node updates/s of K1 vs the MUFU (XU) pipe bound: 148 SM x 16 MUFU/clk x sm_max_mhz / "
                 "4 MUFU per g; HBM is <1% (4.2 KB/frame)",
         "peak_at_measured_clock": (sms * 16 * ck["sm_mhz"] * 1e6 / 4 / 1e9) if ck.get("sm_mhz") else None,
@@ -291,7 +291,7 @@ def run_gpu(args):
         import oracle
 
         threads = oracle.cpu_count()
-        fpp = args.cpu_frames or max(128, 8 * threads)
+        fpp = args.cpu_frames or max(256, 24 * threads)
         v, busy = cpu_hybrid_sample(fpp, threads)
         cpu = {"value": v, "unit": "Gbit/s", "cores": threads, "kind": "port",
                "sample": f"{fpp} frames per Eb/N0 point x {len(EBNO)} points, {busy:.1f} s of CPU wall "

@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
     extern __shared__ __align__(16) uint32_t smw[];
     const int N = a.code.N, n = a.code.n, tp = a.tp, ss = a.ss, psw = a.psw, uhs = a.uhs;
     const int NW = (N + 31) >> 5;
+    const int K = a.code.k, KW = (K + 31) >> 5;
     uint32_t *frz = smw;      // CTA-shared frozen mask
     uint32_t *dam = smw + NW; // CTA-shared decision-aided mask
     const int lane = threadIdx.x & 31;
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
             lanepat = set_slot(lanepat, s, lane);
         uint64_t pll = lanepat, ppp = lanepat; // slot pointers: LLR levels, partial-sum levels
         int P = grp_live ? 1 : 0;
+        int ji = 0; // index of the next non-frozen position (decisions are stored per info index)
         float metric = 0.0f;
 
         for (int i = 0; i < N; ++i) {
@@ -427,11 +429,16 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
                         cg[L + pl] = c1;
                         __syncwarp();
                         int lt0 = 0, lt1 = 0;
+                        if constexpr (2 * L >= 4) {
 #pragma unroll
-                        for (int j = 0; j < 2 * L; j += 4) {
-                            const float4 v = *reinterpret_cast<const float4 *>(cg + j);
-                            lt0 += (v.x < c0) + (v.y < c0) + (v.z < c0) + (v.w < c0);
-                            lt1 += (v.x < c1) + (v.y < c1) + (v.z < c1) + (v.w < c1);
+                            for (int j = 0; j < 2 * L; j += 4) {
+                                const float4 v = *reinterpret_cast<const float4 *>(cg + j);
+                                lt0 += (v.x < c0) + (v.y < c0) + (v.z < c0) + (v.w < c0);
+                                lt1 += (v.x < c1) + (v.y < c1) + (v.z < c1) + (v.w < c1);
+                            }
+                        } else {
+                            lt0 = (cg[0] < c0) + (cg[1] < c0);
+                            lt1 = (cg[0] < c1) + (cg[1] < c1);
                         }
                         // no ties among the 2P finite candidates <=> their strict ranks sum to fc(fc-1)/2
                         int sum = (act ? lt0 + lt1 : 0);
@@ -479,7 +486,7 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
                         pll = ((uint64_t)pl_hi << 32) | pl_lo;
                         ppp = ((uint64_t)pp_hi << 32) | pp_lo;
                         const uint32_t *from = uh + src * uhs;
-                        for (int w = 0; w <= (i >> 5); ++w)
+                        for (int w = 0; w <= (ji >> 5); ++w)
                             urow[w] = from[w];
                     }
                     P = P == 0 ? 0 : P - nf + nd;
@@ -487,9 +494,12 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
                 }
             }
             if (pl < P) {
-                // record the decision, then fold it into the partial sums
-                const uint32_t bm = 1u << (i & 31);
-                urow[i >> 5] = u ? (urow[i >> 5] | bm) : (urow[i >> 5] & ~bm);
+                // record the decision (info positions only: frozen bits are 0),
+                // then fold it into the partial sums
+                if (!fz) {
+                    const uint32_t bm = 1u << (ji & 31);
+                    urow[ji >> 5] = u ? (urow[ji >> 5] | bm) : (urow[ji >> 5] & ~bm);
+                }
                 const int S = __ffs(~i) - 1; // trailing ones of i
                 if (S < n) {
                     uint32_t F5 = u;
@@ -515,6 +525,7 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
                     ppp = set_slot(ppp, S, lane);
                 }
             }
+            ji += fz ? 0 : 1;
             __syncwarp();
         }
 
@@ -523,14 +534,14 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
         bool ok = false;
         if (act && a.code.crc_width > 0) {
             uint32_t syn = 0;
-            for (int w = 0; w < NW; ++w) {
+            for (int w = 0; w < KW; ++w) {
                 uint32_t v = urow[w];
-                if (32 * w + 32 > N)
-                    v &= (1u << (N & 31)) - 1u;
+                if (32 * w + 32 > K)
+                    v &= (1u << (K & 31)) - 1u;
                 while (v) {
                     const int b = __ffs(v) - 1;
                     v &= v - 1u;
-                    syn ^= __ldg(a.code.crc_cols + 32 * w + b);
+                    syn ^= __ldg(a.code.crc_cols + __ldg(a.code.info_pos + 32 * w + b));
                 }
             }
             ok = syn == a.code.crc_offset;
@@ -552,17 +563,22 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
             const uint32_t *row = uh + (gbase + who) * uhs;
             if (a.u_bits != nullptr)
                 for (int w = pl; w < NW; w += L) {
-                    uint32_t v = row[w];
-                    if (32 * w + 32 > N)
-                        v &= (1u << (N & 31)) - 1u;
+                    // scatter the info bits back to block positions (frozen = 0)
+                    int rank = 32 * w;
+                    for (int z = 0; z < w; ++z)
+                        rank -= __popc(frz[z]);
+                    uint32_t v = 0;
+                    for (int b = 0; b < 32 && 32 * w + b < N; ++b)
+                        if (!((frz[w] >> b) & 1u))
+                            v |= bitw(row, rank++) << b;
                     a.u_bits[(size_t)frame * NW + w] = v;
                 }
             if (a.payload != nullptr) {
                 const int MW = (a.code.m + 31) >> 5;
                 for (int w = pl; w < MW; w += L) {
-                    uint32_t v = 0;
-                    for (int b = 0; b < 32 && 32 * w + b < a.code.m; ++b)
-                        v |= bitw(row, __ldg(a.code.info_pos + 32 * w + b)) << b;
+                    uint32_t v = row[w]; // payload = the first m info bits
+                    if (32 * w + 32 > a.code.m)
+                        v &= (1u << (a.code.m & 31)) - 1u;
                     a.payload[(size_t)frame * MW + w] = v;
                 }
             }
@@ -591,14 +607,15 @@ int scl_prepare(SclArgs &a, int nv_req)
         nv = 0;
     if (nv > n - 2)
         nv = n - 2 > 0 ? n - 2 : 0; // keep at least levels 0..1 stored (float4 needs tp >= 2 anyway)
-    if (nv > 3)
-        nv = 3;
+    if (nv > 4)
+        nv = 4;
     a.nv = nv;
     a.tp = n - 1 - nv;
     a.ss = (1 << (a.tp + 1)) + 4;
     a.psw = ps_off(n) | 1; // words for levels 0..n-1, odd stride
     const int nw = (a.code.N + 31) >> 5;
-    a.uhs = nw | 1;
+    (void)nw;
+    a.uhs = ((a.code.k + 31) >> 5) | 1; // decisions at the k non-frozen positions
     a.table_words = (2 * nw + 3) & ~3;
     return PC_OK;
 }
@@ -644,6 +661,7 @@ static int launch_scl_nv(const SclArgs &a, int wpc, int max_warps, cudaStream_t 
     case 1: return launch_scl_t<L, FEX, 1>(a, wpc, max_warps, s);
     case 2: return launch_scl_t<L, FEX, 2>(a, wpc, max_warps, s);
     case 3: return launch_scl_t<L, FEX, 3>(a, wpc, max_warps, s);
+    case 4: return launch_scl_t<L, FEX, 4>(a, wpc, max_warps, s);
     default: return PC_ERR_UNSUPPORTED;
     }
 }

@@ -177,7 +177,10 @@ class HybridDecoder:
         self.stamps = torch.zeros((self.nchunks_max, 4), dtype=torch.int64, **z)
         self.workspaces = torch.zeros((self.nchunks_max, 64), dtype=torch.int32, **z)
         self.s_bp = torch.cuda.Stream(device=dev)
-        self.s_scl = torch.cuda.Stream(device=dev) if overlap else self.s_bp
+        # The list decoder's persistent warps get the higher stream priority, so
+        # they take SM slots as soon as K1 CTAs (one frame each) retire and the
+        # two kernels share the GPU instead of running back to back.
+        self.s_scl = torch.cuda.Stream(device=dev, priority=-1) if overlap else self.s_bp
         self.kernel_events = None  # set to [] to time every K1 launch with CUDA events on the BP stream
         self.launches_per_chunk = 7  # 4 stamp kernels + K1 + K2 + K3 (memset nodes not counted)
         self._llr_dev = None

@@ -65,7 +65,7 @@ class SclConfig:
             int(self.f_mode == "exact"),
             int(self.selector == "bitonic"),
             nat.env_int("PC_SCL_NV", -1) if virtual_levels is None else virtual_levels,
-            warps_per_cta or nat.env_int("PC_SCL_WPC", 2),
+            warps_per_cta or nat.env_int("PC_SCL_WPC", 1),
         )
 
 
