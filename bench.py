@@ -150,6 +150,7 @@ def run_gpu(args):
     from paper_1609_09358_b200 import BpConfig, CodeConfig, HybridDecoder, SclConfig
     from paper_1609_09358_b200 import _native as nat
     from paper_1609_09358_b200.channel import ebno_to_sigma
+    from paper_1609_09358_b200.shard import max_over_ranks, shard_range
 
     lib = nat.load()
     code = CodeConfig(N, K, crc=16)
@@ -163,7 +164,8 @@ def run_gpu(args):
     msg = torch.empty((len(EBNO), B, MW), dtype=torch.int32, device=dev)
     for p, eb in enumerate(EBNO):
         sigma = ebno_to_sigma(eb, code.rate)
-        nat.check(lib.pc_gen_frames(SEED, p, rank * B, B, sigma, dc.ref, msg[p].data_ptr(), llr[p].data_ptr(),
+        nat.check(lib.pc_gen_frames(SEED, p, shard_range(rank, world, B)[0], B, sigma, dc.ref, msg[p].data_ptr(),
+                                    llr[p].data_ptr(),
                                     nat.stream_handle()), "pc_gen_frames")
     dec = HybridDecoder(code, BpConfig(i_max=IMAX), SclConfig(LIST), capacity=B, chunk=args.chunk or B)
     errs = torch.zeros((len(EBNO), 2), dtype=torch.int64, device=dev)
@@ -225,10 +227,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     errs_h = errs.cpu().numpy()
 
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = max_over_ranks(elapsed_ms, device=dev)
     bits_step = B * m * len(EBNO)
     value = world * bits_step * args.steps / (max_ms * 1e-3) / 1e9
 
@@ -279,10 +278,7 @@ def run_gpu(args):
                 dec.decode_host(host[p])
         barrier()
         e2e_s = time.perf_counter() - t0
-        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_val = world * bits_step * args.steps / float(te.item()) / 1e9
+        e2e_val = world * bits_step * args.steps / max_over_ranks(e2e_s, device=dev) / 1e9
     h2d = B * N * 4 * len(EBNO)
     d2h = B * (MW * 4 + 1) * len(EBNO)
 

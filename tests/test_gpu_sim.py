@@ -1,0 +1,52 @@
+"""The Monte Carlo driver (sim.run_sweep) on the device decoders against the
+reference's own committed simulator outputs (plot-tool fixtures, golden_meta
+"fixtures"): same keyed frames, same stopping rule, so the non-timing columns
+must reproduce.  BP-only points may differ on near-tie frames (fp32 vs fp64
+past ~20 iterations); those rows are held to a small tolerance."""
+
+import pytest
+
+from paper_1609_09358_b200 import SimConfig, run_sweep
+
+pytestmark = pytest.mark.gpu
+
+
+def _parse(cfgline):
+    kw = {}
+    for item in cfgline.split():
+        k, v = item.split("=", 1)
+        if k == "ebno_points":
+            kw[k] = tuple(float(x) for x in v.split(":"))
+        elif k in ("frozen_file",):
+            kw[k] = None if v == "None" else v
+        elif v in ("True", "False"):
+            kw[k] = v == "True"
+        else:
+            try:
+                kw[k] = int(v)
+            except ValueError:
+                try:
+                    kw[k] = float(v)
+                except ValueError:
+                    kw[k] = v
+    return SimConfig(**kw)
+
+
+@pytest.mark.parametrize("name", ["hybrid_sweep", "scl_sweep", "no_timing", "bp_sweep"])
+def test_sweep_reproduces_reference_fixture(golden_meta, name):
+    fx = golden_meta["fixtures"][name]
+    cfg = _parse(fx["config"])
+    recs = run_sweep(cfg)
+    assert len(recs) == len(fx["rows"])
+    for rec, row in zip(recs, fx["rows"]):
+        assert rec.ebno_db == float(row["ebno_db"])
+        if cfg.decoder == "bp":
+            # near-tie BP frames may move the stopping point by a frame or two
+            assert abs(rec.frames - int(row["frames"])) <= max(2, int(0.01 * int(row["frames"]))), (rec, row)
+            assert abs(rec.frame_errors - int(row["frame_errors"])) <= 1, (rec, row)
+            continue
+        assert rec.frames == int(row["frames"]), (rec, row)
+        assert rec.frame_errors == int(row["frame_errors"]), (rec, row)
+        assert rec.bit_errors == int(row["bit_errors"]), (rec, row)
+        if row["gamma_bp_fer"]:
+            assert abs(rec.gamma_bp_fer - float(row["gamma_bp_fer"])) <= 2.0 / rec.frames, (rec, row)
