@@ -132,7 +132,7 @@ int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32
     a.work = reinterpret_cast<int32_t *>(workspace);
     int nv = cfg->virtual_levels;
     if (nv < 0)
-        nv = code->n >= 10 ? 3 : (code->n >= 8 ? 2 : 0);
+        nv = code->n >= 12 ? 4 : (code->n >= 10 ? 3 : (code->n >= 8 ? 2 : 0));
     scl_prepare(a, nv);
     return launch_scl(a, L, cfg->warps_per_cta, (cudaStream_t)stream);
 }

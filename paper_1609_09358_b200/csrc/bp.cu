@@ -242,16 +242,21 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
 }
 
 // Teacher-forced hook: one full iterate_once on explicit [B][n+1][N] state.
-template <int GMODE>
+// SMEM = true stages the frame's state in shared memory (N <= 2048); for
+// N = 4096 (426 KB of state) the same sweeps run in place on global memory.
+template <int GMODE, bool SMEM>
 __global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float lim)
 {
     extern __shared__ __align__(16) float st[];
     const int N = 1 << n;
-    float *L = st, *R = st + (size_t)(n + 1) * N;
     const size_t base = (size_t)blockIdx.x * (n + 1) * N;
-    for (int i = threadIdx.x; i < (n + 1) * N; i += blockDim.x) {
-        L[i] = l_msgs[base + i];
-        R[i] = r_msgs[base + i];
+    float *L = SMEM ? st : l_msgs + base;
+    float *R = SMEM ? st + (size_t)(n + 1) * N : r_msgs + base;
+    if (SMEM) {
+        for (int i = threadIdx.x; i < (n + 1) * N; i += blockDim.x) {
+            L[i] = l_msgs[base + i];
+            R[i] = r_msgs[base + i];
+        }
     }
     __syncthreads();
     const int NPE = N / 2;
@@ -277,9 +282,11 @@ __global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float lim)
         }
         __syncthreads();
     }
-    for (int i = threadIdx.x; i < (n + 1) * N; i += blockDim.x) {
-        l_msgs[base + i] = L[i];
-        r_msgs[base + i] = R[i];
+    if (SMEM) {
+        for (int i = threadIdx.x; i < (n + 1) * N; i += blockDim.x) {
+            l_msgs[base + i] = L[i];
+            r_msgs[base + i] = R[i];
+        }
     }
 }
 
@@ -361,7 +368,12 @@ int launch_bp_iterate(float *l, float *r, int B, int n, int g_mode, float lim, c
         return PC_OK;
     const size_t smem = (size_t)2 * (n + 1) * ((size_t)1 << n) * sizeof(float);
     const int threads = (1 << (n - 1)) >= 256 ? 256 : (1 << (n - 1));
-    auto kern = g_mode == 0 ? k_bp_iterate<0> : k_bp_iterate<1>;
+    if (smem > 200 * 1024) {
+        auto kern = g_mode == 0 ? k_bp_iterate<0, false> : k_bp_iterate<1, false>;
+        kern<<<B, threads, 0, s>>>(l, r, n, lim);
+        return cudaGetLastError() == cudaSuccess ? PC_OK : PC_ERR_CUDA;
+    }
+    auto kern = g_mode == 0 ? k_bp_iterate<0, true> : k_bp_iterate<1, true>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return PC_ERR_CUDA;
     kern<<<B, threads, smem, s>>>(l, r, n, lim);

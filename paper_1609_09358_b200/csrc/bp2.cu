@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
     constexpr int NW = (N + 31) / 32;
     constexpr int NWARP = TPF / 32;
     constexpr int PPT = N / 2 / TPF; // shared-memory boundary elements per thread
-    static_assert(TPF >= 32 && Q >= 2 && Q <= 32 && BW <= LOGN, "bp2 geometry");
+    static_assert(TPF >= 32 && Q >= 2 && Q <= 8 && BW <= LOGN, "bp2 geometry");
 
     extern __shared__ __align__(16) float sm[];
     float *Rs = sm;           // R[BW + r], r < NSR
@@ -286,10 +286,10 @@ template <int LOGN, int GMODE>
 static int launch_bp2_n(const BpArgs &a, int tpf, cudaStream_t s)
 {
     constexpr int N = 1 << LOGN;
-    constexpr int LO = N / 32 > 32 ? N / 32 : 32; // Q <= 32 nodes per thread
-    constexpr int HI = N / 2;                     // Q >= 2
+    constexpr int LO = N / 8 > 32 ? N / 8 : 32; // Q <= 8 nodes per thread (Q = 16 needs ~120+ registers)
+    constexpr int HI = N / 2;                   // Q >= 2
     if (tpf <= 0)
-        tpf = N / 4 >= 256 ? 256 : N / 4;
+        tpf = N >= 4096 ? 1024 : (N / 4 >= 256 ? 256 : N / 4);
     if (tpf < LO || tpf > HI)
         return PC_ERR_UNSUPPORTED;
 #define PC_BP2_CASE(T)                                                                                                 \
@@ -306,12 +306,13 @@ static int launch_bp2_n(const BpArgs &a, int tpf, cudaStream_t s)
 #undef PC_BP2_CASE
 }
 
-// K1 v2 covers N = 128 .. 2048 with the crc / none stop rules and no soft_x.
+// K1 v2 covers N = 128 .. 4096 with the crc / none stop rules and no soft_x.
+// N = 4096 runs one 1024-thread CTA per frame (Q = 4): 11 shared rows, 176 KB.
 bool bp2_eligible(const BpArgs &a, int tpf)
 {
     const int N = a.code.N;
-    const int lo = N / 32 > 32 ? N / 32 : 32;
-    return a.code.n >= 7 && a.code.n <= 11 && a.stop_mode != 1 && a.soft_x == nullptr &&
+    const int lo = N / 8 > 32 ? N / 8 : 32;
+    return a.code.n >= 7 && a.code.n <= 12 && a.stop_mode != 1 && a.soft_x == nullptr &&
            (tpf <= 0 || (tpf >= lo && tpf <= N / 2));
 }
 
@@ -327,6 +328,7 @@ int launch_bp2(const BpArgs &a, int g_mode, int tpf, cudaStream_t s)
         case 9: return launch_bp2_n<9, 0>(a, tpf, s);
         case 10: return launch_bp2_n<10, 0>(a, tpf, s);
         case 11: return launch_bp2_n<11, 0>(a, tpf, s);
+        case 12: return launch_bp2_n<12, 0>(a, tpf, s);
         }
     } else {
         switch (n) {
@@ -335,6 +337,7 @@ int launch_bp2(const BpArgs &a, int g_mode, int tpf, cudaStream_t s)
         case 9: return launch_bp2_n<9, 1>(a, tpf, s);
         case 10: return launch_bp2_n<10, 1>(a, tpf, s);
         case 11: return launch_bp2_n<11, 1>(a, tpf, s);
+        case 12: return launch_bp2_n<12, 1>(a, tpf, s);
         }
     }
     return PC_ERR_UNSUPPORTED;

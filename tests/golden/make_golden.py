@@ -79,7 +79,8 @@ def main():
 
     # ---- BP with the CRC stop -------------------------------------------------
     bp_sets = [("bp128", 128, 64, 2.0, 11, 300), ("bp1024a", 1024, 512, 1.5, 12, 60),
-               ("bp1024b", 1024, 512, 2.5, 13, 60), ("bp2048", 2048, 1024, 2.0, 14, 12)]
+               ("bp1024b", 1024, 512, 2.5, 13, 60), ("bp2048", 2048, 1024, 2.0, 14, 12),
+               ("bp4096", 4096, 2048, 2.0, 17, 16)]
     meta = {}
     for name, N, k, eb, seed, cnt in bp_sets:
         c = ref.CodeConfig(N, k, crc=16)
@@ -123,7 +124,9 @@ def main():
     scl_sets = [("scl128L4", 128, 64, 4, 1.5, 21, 200), ("scl128L32", 128, 64, 32, 1.0, 22, 100),
                 ("scl1024L8", 1024, 512, 8, 1.5, 23, 40), ("scl1024L32", 1024, 512, 32, 1.5, 24, 40),
                 ("scl2048L32", 2048, 1024, 32, 2.0, 25, 8), ("scl256L1", 256, 128, 1, 1.0, 26, 100),
-                ("scl512L2", 512, 256, 2, 1.5, 27, 60), ("scl512L16", 512, 256, 16, 1.5, 28, 30)]
+                ("scl512L2", 512, 256, 2, 1.5, 27, 60), ("scl512L16", 512, 256, 16, 1.5, 28, 30),
+                ("scl2048L1", 2048, 1024, 1, 1.5, 33, 30), ("scl2048L4", 2048, 1024, 4, 1.5, 34, 20),
+                ("scl4096L8", 4096, 2048, 8, 1.5, 35, 6)]
     for name, N, k, Lsz, eb, seed, cnt in scl_sets:
         c = ref.CodeConfig(N, k, crc=16)
         _, L = frames(c, eb, seed, 0, cnt)

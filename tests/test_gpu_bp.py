@@ -44,7 +44,8 @@ def BpGraph_from(L, R):
     return BpGraph(np.array(L, dtype=np.float64), np.array(R, dtype=np.float64))
 
 
-@pytest.mark.parametrize("N,g_mode", [(4, "exact"), (8, "min"), (128, "exact"), (128, "min"), (2048, "exact")])
+@pytest.mark.parametrize("N,g_mode", [(4, "exact"), (8, "min"), (128, "exact"), (128, "min"), (2048, "exact"),
+                                      (4096, "exact"), (4096, "min")])
 def test_teacher_forced_iterations_vs_oracle(N, g_mode):
     """Five iterations, each restarted from the oracle's own state (teacher forcing)."""
     code = CodeConfig(N, N // 2, crc=None)
@@ -87,7 +88,7 @@ def _check_decisions(name, ref_u, ref_it, ref_cv, got):
     return late
 
 
-@pytest.mark.parametrize("name", ["bp128", "bp1024a", "bp1024b", "bp2048"])
+@pytest.mark.parametrize("name", ["bp128", "bp1024a", "bp1024b", "bp2048", "bp4096"])
 def test_crc_stop_decisions_match_reference(golden, golden_meta, name):
     meta = golden_meta["sets"][name]
     code = CodeConfig(meta["N"], meta["k"], crc=16)
@@ -126,6 +127,47 @@ def test_crc_stop_vs_oracle_at_scale():
     got = bp_decode_batch(llrs, code, BpConfig(i_max=50, stop_mode="crc"))
     late = _check_decisions("oracle2000", ref_u, ref_it, ref_cv, got)
     print("near-tie frames:", late)
+
+
+@pytest.mark.parametrize("eb", [2.0, 3.0])
+def test_n4096_crc_stop_vs_oracle(eb):
+    """C4 (N=4096 K=2048): the 1024-thread-per-frame register/shuffle kernel
+    against the C oracle on identical fp32 inputs."""
+    code = CodeConfig(4096, 2048, crc=16)
+    sigma = ebno_to_sigma(eb, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(4096, int(eb * 10), f))[1] for f in range(96)])
+    llrs = llrs.astype(np.float32).astype(np.float64)
+    ref_u, ref_it, ref_cv = oracle.bp_batch(llrs, code, stop_mode="crc")
+    got = bp_decode_batch(llrs, code, BpConfig(i_max=50, stop_mode="crc"))
+    late = _check_decisions(f"N4096-{eb}", ref_u, ref_it, ref_cv, got)
+    print("near-tie frames:", late)
+
+
+@pytest.mark.parametrize("N,eb,count", [(4096, 2.5, 12), (1024, 2.0, 40)])
+def test_minsum_bit_exact_vs_fp32_restatement(N, eb, count):
+    """g_mode="min": min, sign, clip and fp32 adds only, so the device equals a
+    literal fp32 restatement bit for bit (iterations, flags, u_hat).  Against
+    the fp64 oracle min-sum drifts from ~13 iterations (tests/fp32_bp.py)."""
+    from fp32_bp import bp_minsum_f32
+
+    code = CodeConfig(N, N // 2, crc=16)
+    sigma = ebno_to_sigma(eb, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(4096, int(eb * 10), f))[1] for f in range(count)])
+    llrs = llrs.astype(np.float32).astype(np.float64)
+    got = bp_decode_batch(llrs, code, BpConfig(i_max=50, g_mode="min", stop_mode="crc"))
+    for f in range(count):
+        u, it, cv = bp_minsum_f32(llrs[f], code)
+        assert (int(got.iterations_used[f]), bool(got.converged[f])) == (it, cv), f"frame {f}"
+        assert np.array_equal(got.u_hat[f], u), f"frame {f}"
+
+
+def test_n4096_unsupported_paths_fail_loudly():
+    """N=4096 state does not fit one SM for the shared-memory kernel: the
+    re-encode stop and soft_x raise instead of silently falling back."""
+    code = CodeConfig(4096, 2048, crc=16)
+    llrs = np.zeros((2, 4096))
+    with pytest.raises(RuntimeError):
+        bp_decode_batch(llrs, code, BpConfig(stop_mode="reencode"))
 
 
 def test_single_frame_api_and_soft_outputs():

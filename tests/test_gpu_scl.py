@@ -26,7 +26,8 @@ def _compare(name, ref_u, ref_metric, ref_crc, got, allow=0):
 
 
 @pytest.mark.parametrize(
-    "name", ["scl128L4", "scl128L32", "scl1024L8", "scl1024L32", "scl2048L32", "scl256L1", "scl512L2", "scl512L16"]
+    "name", ["scl128L4", "scl128L32", "scl1024L8", "scl1024L32", "scl2048L32", "scl256L1", "scl512L2", "scl512L16",
+             "scl2048L1", "scl2048L4", "scl4096L8"]
 )
 def test_winners_match_reference(golden, golden_meta, name):
     meta = golden_meta["sets"][name]

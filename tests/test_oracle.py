@@ -14,7 +14,7 @@ from paper_1609_09358_b200.channel import ebno_to_sigma, frame_rng, make_frame
 
 
 def test_bp_decisions_match_golden(golden, golden_meta):
-    for name in ("bp128", "bp1024a", "bp1024b", "bp2048"):
+    for name in ("bp128", "bp1024a", "bp1024b", "bp2048", "bp4096"):
         meta = golden_meta["sets"][name]
         code = CodeConfig(meta["N"], meta["k"], crc=16)
         _, llrs = golden_frames(meta, code)
@@ -50,7 +50,7 @@ def test_g_known_values():
 
 def test_scl_winners_match_golden(golden, golden_meta):
     for name in ("scl128L4", "scl128L32", "scl1024L8", "scl1024L32", "scl2048L32", "scl256L1", "scl512L2",
-                 "scl512L16"):
+                 "scl512L16", "scl2048L1", "scl2048L4", "scl4096L8"):
         meta = golden_meta["sets"][name]
         code = CodeConfig(meta["N"], meta["k"], crc=16)
         _, llrs = golden_frames(meta, code)
