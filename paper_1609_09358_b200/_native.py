@@ -72,6 +72,7 @@ class PcSclCfg(C.Structure):
         ("selector_bitonic", C.c_int32),
         ("virtual_levels", C.c_int32),
         ("warps_per_cta", C.c_int32),
+        ("kernel", C.c_int32),
     ]
 
 

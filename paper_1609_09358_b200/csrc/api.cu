@@ -130,7 +130,19 @@ int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32
     a.sel = sel_by_crc;
     a.t_done = t_done;
     a.work = reinterpret_cast<int32_t *>(workspace);
+    if (cfg->kernel < 0 || cfg->kernel > 2)
+        return PC_ERR_INVALID;
     int nv = cfg->virtual_levels;
+    if (cfg->kernel != 1 && scl3_eligible(a, L)) {
+        if (nv < 0)
+            nv = code->n >= 12 ? 4 : (code->n >= 10 ? 3 : (code->n >= 8 ? 2 : 0));
+        const int rc3 = scl3_prepare(a, L, nv);
+        if (rc3)
+            return rc3;
+        return launch_scl3(a, L, cfg->warps_per_cta, (cudaStream_t)stream);
+    }
+    if (cfg->kernel == 2)
+        return PC_ERR_UNSUPPORTED;
     if (nv < 0)
         nv = code->n >= 12 ? 4 : (code->n >= 10 ? 3 : (code->n >= 8 ? 2 : 0));
     scl_prepare(a, nv);

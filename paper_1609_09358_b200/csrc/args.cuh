@@ -36,6 +36,8 @@ struct SclArgs {
     int32_t uhs;     // decision slot stride (words)
     int32_t warp_words;  // per-warp shared words (slots, partial sums, decisions, candidates, channel)
     int32_t table_words; // CTA-shared frozen / decision-aided masks
+    // v3 (scl3.cu) per-warp section offsets, in 32-bit words from the warp base
+    int32_t o_ps, o_tb, o_tba, o_cand, o_wrow, o_ch;
 };
 
 int launch_bp_decode(const BpArgs &a, int g_mode, int tpf, int kernel, cudaStream_t s);
@@ -44,6 +46,9 @@ int launch_bp2(const BpArgs &a, int g_mode, int tpf, cudaStream_t s);
 int launch_bp_iterate(float *l, float *r, int B, int n, int g_mode, float lim, cudaStream_t s);
 int scl_prepare(SclArgs &a, int nv_req);
 int launch_scl(const SclArgs &a, int L, int wpc, cudaStream_t s);
+bool scl3_eligible(const SclArgs &a, int L);
+int scl3_prepare(SclArgs &a, int L, int nv_req);
+int launch_scl3(const SclArgs &a, int L, int wpc, cudaStream_t s);
 int launch_compact(const uint8_t *conv, int B, int32_t *queue, int32_t *count, cudaStream_t s);
 int launch_gen(const Code &c, uint64_t seed, int point, int64_t frame0, int B, float sigma, uint32_t *msg, float *llr,
                cudaStream_t s);

@@ -1,0 +1,605 @@
+// scl3.cuh -- K3 v3: CRC-aided SCL with register-resident leaf blocks (sm_100a).
+//
+// Same decoder as scl.cu (reference _kernels.py:144-333 + scl.py:177-191, with
+// the reference's logical slot numbering and (metric, candidate index) order),
+// restructured around blocks of 2^T = 8 leaves:
+//
+//   * upper descent, once per block: tree levels >= T+1 live in shared memory
+//     with lazy slot pointers (as in v2) and produce the block's level-T LLRs
+//     straight into registers;
+//   * the 8 leaves of a block run fully unrolled on registers: levels 0..T-1,
+//     the partial sums of those levels (one word) and all per-leaf control are
+//     compile-time.  A clone copies the parent's still-readable register
+//     levels with shuffles (the reference's eager copy, _kernels.py:288-303);
+//   * survivor selection at a full list (P == L): the agreeing children start
+//     as survivors and the best excluded candidate is swapped for the worst
+//     kept one until no excluded candidate beats a kept one.  Each round is
+//     two warp reductions (redux.sync at L = 32); the common reliable position
+//     exits after the first round.  The result is exactly the L smallest
+//     (metric, index) pairs (_kernels.py:253-267);
+//   * the CRC syndrome of every path is carried incrementally (one XOR of the
+//     position's syndrome column per decided 1) and copied on clone, so the
+//     CRC-aided winner rule (scl.py:181-191) needs no stored decisions;
+//   * decisions are stored as 32-bit windows with an ancestor lane per window
+//     (a traceback); only the winner's path is reconstructed at the end.
+#pragma once
+#include "args.cuh"
+#include "scl_math.cuh"
+#include "scl3_decl.cuh"
+
+namespace pc {
+
+namespace s3 {
+
+
+__device__ __forceinline__ int sl32(uint32_t p, int s) { return (int)((p >> (5 * (s - T - 1))) & 31u); }
+__device__ __forceinline__ uint32_t set32(uint32_t p, int s, int v)
+{
+    const int sh = 5 * (s - T - 1);
+    return (p & ~(31u << sh)) | ((uint32_t)v << sh);
+}
+__device__ __forceinline__ int sl64(uint64_t p, int s) { return (int)((p >> (5 * (s - T))) & 31u); }
+__device__ __forceinline__ uint64_t set64(uint64_t p, int s, int v)
+{
+    const int sh = 5 * (s - T);
+    return (p & ~(31ull << sh)) | ((uint64_t)v << sh);
+}
+
+// compile-time trailing zeros / ones of a small non-negative integer
+__host__ __device__ constexpr int ctz_c(int v) { return (v & 1) ? 0 : 1 + ctz_c(v >> 1); }
+__host__ __device__ constexpr int cto_c(int v) { return (v & 1) ? 1 + cto_c(v >> 1) : 0; }
+
+// Order-preserving key of a non-negative fp32 metric (metrics only grow from 0).
+__device__ __forceinline__ uint32_t mkey(float m) { return __float_as_uint(m); }
+
+template <int L>
+__device__ __forceinline__ uint32_t gmax_u(uint32_t v)
+{
+    if constexpr (L == 32) {
+        return __reduce_max_sync(0xffffffffu, v);
+    } else {
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1)
+            v = max(v, (uint32_t)__shfl_xor_sync(0xffffffffu, v, off));
+        return v;
+    }
+}
+
+template <int L>
+__device__ __forceinline__ uint32_t gmin_u(uint32_t v)
+{
+    if constexpr (L == 32) {
+        return __reduce_min_sync(0xffffffffu, v);
+    } else {
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1)
+            v = min(v, (uint32_t)__shfl_xor_sync(0xffffffffu, v, off));
+        return v;
+    }
+}
+
+template <int L>
+__device__ __forceinline__ int gmax_i(int v)
+{
+    if constexpr (L == 32) {
+        return __reduce_max_sync(0xffffffffu, v);
+    } else {
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1)
+            v = max(v, __shfl_xor_sync(0xffffffffu, v, off));
+        return v;
+    }
+}
+
+template <int L>
+__device__ __forceinline__ int gmin_i(int v)
+{
+    if constexpr (L == 32) {
+        return __reduce_min_sync(0xffffffffu, v);
+    } else {
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1)
+            v = min(v, __shfl_xor_sync(0xffffffffu, v, off));
+        return v;
+    }
+}
+
+} // namespace s3
+
+template <int L, bool FEX, int NV>
+__global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
+{
+    using namespace s3;
+    constexpr int F = 32 / L;
+    constexpr uint32_t FULL = 0xffffffffu;
+    extern __shared__ __align__(16) uint32_t smw[];
+    const int N = a.code.N, n = a.code.n, tp = a.tp, ss = a.ss, psw = a.psw, W = a.uhs;
+    const int lane = threadIdx.x & 31;
+    uint32_t *wb = smw + (size_t)(threadIdx.x >> 5) * a.warp_words;
+    float *llr = reinterpret_cast<float *>(wb);
+    uint32_t *ps = wb + a.o_ps;
+    uint32_t *tb = wb + a.o_tb;
+    uint8_t *tba = reinterpret_cast<uint8_t *>(wb + a.o_tba);
+    float *cand = reinterpret_cast<float *>(wb + a.o_cand);
+    uint32_t *wrow = wb + a.o_wrow;
+    float *chs = reinterpret_cast<float *>(wb + a.o_ch);
+    const bool ch_smem = a.o_ch >= 0;
+
+    const int grp = lane / L, gbase = grp * L, pl = lane - gbase;
+    const uint32_t gmask_lo = (L == 32) ? FULL : ((1u << L) - 1u);
+    const int total = a.count != nullptr ? *a.count : a.B;
+    float *own = llr + lane * ss;
+    uint32_t *pown = ps + lane * psw;
+    float *cg = cand + grp * 4 * L;
+    const uint32_t *frzg = a.code.frozen_bits;
+    const uint32_t *damg = a.code.da_bits;
+    const uint32_t *colg = a.code.crc_cols;
+    const bool use_crc = a.code.crc_width > 0;
+
+    uint32_t lp32 = 0;
+    uint64_t lp64 = 0;
+    for (int f = 0; f < 6; ++f)
+        lp32 |= (uint32_t)lane << (5 * f);
+    for (int f = 0; f < 12; ++f)
+        lp64 |= (uint64_t)lane << (5 * f);
+
+    for (;;) {
+        int base = 0;
+        if (lane == 0)
+            base = atomicAdd(a.work, F);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= total)
+            break;
+        const int qi = base + grp;
+        const bool grp_live = qi < total;
+        const int frame = grp_live ? (a.queue != nullptr ? a.queue[qi] : qi) : 0;
+        const float *ch;
+        if (ch_smem) {
+            float *mine = chs + grp * N;
+            const float *g = a.llr + (size_t)frame * N;
+            for (int t = 4 * pl; t < N; t += 4 * L)
+                *reinterpret_cast<float4 *>(mine + t) = __ldg(reinterpret_cast<const float4 *>(g + t));
+            ch = mine;
+            __syncwarp();
+        } else {
+            ch = a.llr + (size_t)frame * N;
+        }
+
+        uint32_t pll = lp32; // LLR level pointers, levels T+1..tp
+        uint64_t ppp = lp64; // partial-sum level pointers, levels T..n-1
+        int P = grp_live ? 1 : 0;
+        int ji = 0;
+        float metric = 0.0f;
+        uint32_t syn = 0u, cur = 0u, anc = (uint32_t)lane;
+
+        const int nblk = N >> T;
+        for (int b = 0; b < nblk; ++b) {
+            const int i0 = b << T;
+            const bool act0 = pl < P;
+            // ================= upper descent: level T into registers =================
+            float x[BL];
+            if (act0) {
+                const int start = (b == 0) ? n - 1 : T + __ffs(b) - 1;
+                if (start == T) {
+                    // level T from level T+1 (read through the pointer, or the channel)
+                    const float *src = (T + 1 == n) ? ch : llr + sl32(pll, T + 1) * ss + llo(T + 1);
+                    const uint32_t g = (i0 >> T) & 1u;
+                    const uint32_t bits = g ? ps[sl64(ppp, T) * psw + pso(T)] : 0u;
+#pragma unroll
+                    for (int t = 0; t < BL; t += 4) {
+                        const float4 A = *reinterpret_cast<const float4 *>(src + t);
+                        const float4 Bv = *reinterpret_cast<const float4 *>(src + BL + t);
+                        const float4 o = g ? g4(A, Bv, bits >> t) : f4(A, Bv, FEX);
+                        x[t] = o.x;
+                        x[t + 1] = o.y;
+                        x[t + 2] = o.z;
+                        x[t + 3] = o.w;
+                    }
+                } else {
+                    const int s0 = start < tp ? start : tp;
+                    const int w0 = 1 << s0;
+                    const uint32_t g0 = (i0 >> s0) & 1u;
+                    float *dst = own + llo(s0);
+                    const uint32_t *pw0 = ps + sl64(ppp, s0) * psw + pso(s0);
+                    if (s0 + 1 <= tp) {
+                        const float *src = llr + sl32(pll, s0 + 1) * ss + llo(s0 + 1);
+                        if (g0)
+                            level_from<FEX, true>(dst, src, w0, pw0);
+                        else
+                            level_from<FEX, false>(dst, src, w0, pw0);
+                    } else if (NV == 0) {
+                        if (g0)
+                            level_from<FEX, true>(dst, ch, w0, pw0);
+                        else
+                            level_from<FEX, false>(dst, ch, w0, pw0);
+                    } else {
+                        if constexpr (NV > 0) {
+                            const uint32_t *psp[NV];
+                            uint32_t gm = 0;
+#pragma unroll
+                            for (int d = 0; d < NV; ++d) {
+                                const int r = n - NV + d;
+                                psp[d] = ps + sl64(ppp, r) * psw + pso(r);
+                                gm |= ((uint32_t)(i0 >> r) & 1u) << d;
+                            }
+                            for (int t = 0; t < w0; t += 4) {
+                                const float4 A = virt_top4<NV, FEX>(ch, n, t, psp, gm);
+                                const float4 Bv = virt_top4<NV, FEX>(ch, n, t + w0, psp, gm);
+                                *reinterpret_cast<float4 *>(dst + t) =
+                                    g0 ? g4(A, Bv, pw0[t >> 5] >> (t & 31)) : f4(A, Bv, FEX);
+                            }
+                        }
+                    }
+                    for (int s = s0 - 1; s >= T + 1; --s)
+                        level_from<FEX, false>(own + llo(s), own + llo(s + 1), 1 << s, nullptr);
+                    const float *src = own + llo(T + 1);
+#pragma unroll
+                    for (int t = 0; t < BL; t += 4) {
+                        const float4 o = f4(*reinterpret_cast<const float4 *>(src + t),
+                                            *reinterpret_cast<const float4 *>(src + BL + t), FEX);
+                        x[t] = o.x;
+                        x[t + 1] = o.y;
+                        x[t + 2] = o.z;
+                        x[t + 3] = o.w;
+                    }
+                    for (int s = T + 1; s <= s0; ++s)
+                        pll = set32(pll, s, lane); // levels T+1..s0 now live in the own slot
+                }
+            }
+            __syncwarp();
+            const uint32_t fzw = (__ldg(frzg + (i0 >> 5)) >> (i0 & 31)) & ((1u << BL) - 1u);
+            const uint32_t daw = damg != nullptr ? (__ldg(damg + (i0 >> 5)) >> (i0 & 31)) & ((1u << BL) - 1u) : 0u;
+
+            // ================= the block's leaves, registers only =================
+            static_assert(T == 3, "the leaf code below is written for 8-leaf blocks");
+            float l2[4], l1[2]; // levels 2 and 1 of the block (level 3 is x)
+            uint32_t psr = 0;   // partial sums of levels < T: level s at bits [2^s - 1, 2^(s+1) - 1)
+            uint32_t betaT = 0; // the block's codeword (2^T bits) after its last leaf
+            // One copy of the leaf code for all 8 leaves (runtime j, warp-uniform
+            // branches): an unrolled block overflows the instruction cache.
+#pragma unroll 1
+            for (int j = 0; j < BL; ++j) {
+                // ---- leaf descent: level ctz(j) by g, the levels below by f ----
+                float lam;
+                if (j & 1) {
+                    lam = scl_g(l1[0], l1[1], psr & 1u);
+                } else {
+                    if (j & 2) {
+                        l1[0] = scl_g(l2[0], l2[2], (psr >> 1) & 1u);
+                        l1[1] = scl_g(l2[1], l2[3], (psr >> 2) & 1u);
+                    } else {
+                        if (j & 4) {
+#pragma unroll
+                            for (int t = 0; t < 4; ++t)
+                                l2[t] = scl_g(x[t], x[t + 4], (psr >> (3 + t)) & 1u);
+                        } else {
+#pragma unroll
+                            for (int t = 0; t < 4; ++t)
+                                l2[t] = scl_f<FEX>(x[t], x[t + 4]);
+                        }
+                        l1[0] = scl_f<FEX>(l2[0], l2[2]);
+                        l1[1] = scl_f<FEX>(l2[1], l2[3]);
+                    }
+                    lam = scl_f<FEX>(l1[0], l1[1]);
+                }
+                const int i = i0 + j;
+                const uint32_t fz = (fzw >> j) & 1u;
+                const uint32_t dz = (daw >> j) & 1u;
+                const bool act = pl < P;
+                uint32_t col = 0u;
+                if (!fz && use_crc)
+                    col = __ldg(colg + i);
+                float inc0, inc1;
+                metric_incs(lam, a.metric_exact, inc0, inc1);
+                uint32_t u = 0u;
+                if (fz | dz) {
+                    u = (dz && lam < 0.0f) ? 1u : 0u;
+                    if (act)
+                        metric += u ? inc1 : inc0;
+                } else {
+                    const float c0 = act ? metric + inc0 : INFINITY;
+                    const float c1 = act ? metric + inc1 : INFINITY;
+                    bool k0 = act, k1 = act;
+                    bool need_rank = false;
+                    if (__any_sync(FULL, P == L)) {
+                        // ---- selection at a full list: exactly the L best of 2L by (metric, index) ----
+                        // (live groups share P; a finished group has P = 0 and takes no part)
+                        // g = agreeing child, b = the other.  Every g below the best b is kept and
+                        // every b above the worst g is dropped; the h = #{g >= min b} remaining
+                        // slots go to the h smallest of the uncertain set U = {g >= min b} u {b <= max g}.
+                        const bool z = c0 <= c1; // a tie keeps u = 0 (index p < L + p)
+                        const float gv = z ? c0 : c1, bv = z ? c1 : c0;
+                        const uint32_t gk = mkey(gv), bk = mkey(bv);
+                        const int gi = z ? pl : L + pl, bi = z ? L + pl : pl;
+                        const uint32_t gm = gmax_u<L>(act ? gk : 0u);
+                        const uint32_t bm = gmin_u<L>(act ? bk : FULL);
+                        const bool hiG = act && gk >= bm, loB = act && bk <= gm;
+                        bool inG = act, inB = false;
+                        if (__any_sync(FULL, hiG)) {
+                            const uint32_t gb = (__ballot_sync(FULL, hiG) >> gbase) & gmask_lo;
+                            const uint32_t bb = (__ballot_sync(FULL, loB) >> gbase) & gmask_lo;
+                            const int h = __popc(gb), l = __popc(bb);
+                            // (a group with some g >= min b has h >= 1 and l >= 1)
+                            if (__all_sync(FULL, h <= 1 || l <= 1)) {
+                                // one swap at most: the worst kept g against the best dropped b
+                                const int gx = gmax_i<L>(act && gk == gm ? gi : -1);
+                                const int bx = gmin_i<L>(act && bk == bm ? bi : 2 * L);
+                                if (h > 0 && (bm < gm || (bm == gm && bx < gx))) {
+                                    if (gk == gm && gi == gx)
+                                        inG = false;
+                                    if (bk == bm && bi == bx)
+                                        inB = true;
+                                }
+                            } else {
+                                // rank inside U by the exact (metric, index) key
+                                const uint32_t below = (1u << pl) - 1u;
+                                const int nu = h + l;
+                                unsigned long long *uk = reinterpret_cast<unsigned long long *>(cg);
+                                const unsigned long long kg = ((unsigned long long)gk << 8) | (unsigned)gi;
+                                const unsigned long long kb = ((unsigned long long)bk << 8) | (unsigned)bi;
+                                if (hiG)
+                                    uk[__popc(gb & below)] = kg;
+                                if (loB)
+                                    uk[h + __popc(bb & below)] = kb;
+                                __syncwarp();
+                                int rg = 0, rb = 0;
+                                const int numax = __reduce_max_sync(FULL, nu);
+                                for (int q = 0; q < numax; ++q) {
+                                    const unsigned long long v = q < nu ? uk[q] : ~0ull;
+                                    rg += v < kg;
+                                    rb += v < kb;
+                                }
+                                if (hiG)
+                                    inG = rg < h;
+                                if (loB)
+                                    inB = rb < h;
+                                __syncwarp();
+                            }
+                        }
+                        k0 = z ? inG : inB;
+                        k1 = z ? inB : inG;
+                    } else if (__any_sync(FULL, 2 * P > L)) {
+                        need_rank = true;
+                    }
+                    // ---- slot assignment (_kernels.py:271-311) ----
+                    const uint32_t freeM = (__ballot_sync(FULL, act && !k0 && !k1) >> gbase) & gmask_lo;
+                    const uint32_t dupM = (__ballot_sync(FULL, act && k0 && k1) >> gbase) & gmask_lo;
+                    const int nf = __popc(freeM), nd = __popc(dupM);
+                    int src = lane;
+                    if (act && (k0 || k1)) {
+                        u = k0 ? 0u : 1u;
+                        metric = k0 ? c0 : c1;
+                    } else {
+                        const int r = act ? __popc(freeM & ((1u << pl) - 1u)) : nf + (pl - P);
+                        if (r < nd) {
+                            uint32_t m = dupM; // the r-th set bit of dupM is the parent this slot clones
+                            for (int q = 0; q < r; ++q)
+                                m &= m - 1u;
+                            src = gbase + __ffs(m) - 1;
+                        }
+                    }
+                    if (__any_sync(FULL, src != lane)) {
+                        const float pc1 = __shfl_sync(FULL, c1, src);
+                        // eager copy of the still-readable register levels: level s+1 while
+                        // bit s of j is 0 (the reference's rule at _kernels.py:296-303)
+                        if ((j & 4) == 0) {
+#pragma unroll
+                            for (int t = 0; t < BL; ++t)
+                                x[t] = __shfl_sync(FULL, x[t], src);
+                        }
+                        if ((j & 2) == 0) {
+#pragma unroll
+                            for (int t = 0; t < 4; ++t)
+                                l2[t] = __shfl_sync(FULL, l2[t], src);
+                        }
+                        if ((j & 1) == 0) {
+                            l1[0] = __shfl_sync(FULL, l1[0], src);
+                            l1[1] = __shfl_sync(FULL, l1[1], src);
+                        }
+                        const uint32_t psr2 = __shfl_sync(FULL, psr, src);
+                        const uint32_t pll2 = __shfl_sync(FULL, pll, src);
+                        const uint32_t pp_lo = __shfl_sync(FULL, (uint32_t)ppp, src);
+                        const uint32_t pp_hi = __shfl_sync(FULL, (uint32_t)(ppp >> 32), src);
+                        const uint32_t syn2 = __shfl_sync(FULL, syn, src);
+                        const uint32_t cur2 = __shfl_sync(FULL, cur, src);
+                        const uint32_t anc2 = __shfl_sync(FULL, anc, src);
+                        if (src != lane) {
+                            u = 1u;
+                            metric = pc1;
+                            psr = psr2;
+                            pll = pll2;
+                            ppp = ((uint64_t)pp_hi << 32) | pp_lo;
+                            syn = syn2;
+                            cur = cur2;
+                            anc = anc2;
+                        }
+                    }
+                    P = P == 0 ? 0 : P - nf + nd;
+                }
+                // ---- record the decision (non-frozen positions) ----
+                if (!fz) {
+                    cur |= u << (ji & 31);
+                    syn ^= u ? col : 0u;
+                    ++ji;
+                    if ((ji & 31) == 0) {
+                        const int w = (ji >> 5) - 1;
+                        tb[w * 32 + lane] = cur;
+                        tba[w * 32 + lane] = (uint8_t)anc;
+                        cur = 0u;
+                        anc = (uint32_t)lane;
+                    }
+                }
+                // ---- fold u into the register partial sums: level S = trailing ones of j ----
+                {
+                    uint32_t Fw = u;
+                    if (j & 1) {
+                        Fw = ((psr ^ Fw) & 1u) | (Fw << 1);
+                        if (j & 2) {
+                            Fw = (((psr >> 1) ^ Fw) & 3u) | (Fw << 2);
+                            if (j & 4)
+                                betaT = (((psr >> 3) ^ Fw) & 15u) | (Fw << 4);
+                            else
+                                psr = (psr & ~(15u << 3)) | (Fw << 3);
+                        } else {
+                            psr = (psr & ~(3u << 1)) | (Fw << 1);
+                        }
+                    } else {
+                        psr = (psr & ~1u) | Fw;
+                    }
+                }
+            }
+
+            // ================= block end: fold the block codeword into the shared levels =================
+            if (pl < P) {
+                const int S = T + __ffs(~b) - 1; // level of the node completed by this block
+                if (S < n) {
+                    uint32_t F5 = betaT;
+                    const int lo = S < 5 ? S : 5;
+                    for (int s = T; s < lo; ++s) {
+                        const int len = 1 << s;
+                        const uint32_t pv = ps[sl64(ppp, s) * psw + pso(s)];
+                        F5 = ((pv ^ F5) & ((1u << len) - 1u)) | (F5 << len);
+                    }
+                    uint32_t *dst = pown + pso(S);
+                    if (S <= 5) {
+                        dst[0] = F5;
+                    } else {
+                        const int words = 1 << (S - 5);
+                        for (int w = 0; w < words; ++w) {
+                            uint32_t v = F5;
+                            for (int s = 5; s < S; ++s)
+                                if (((w >> (s - 5)) & 1) == 0)
+                                    v ^= ps[sl64(ppp, s) * psw + pso(s) + (w & ((1 << (s - 5)) - 1))];
+                            dst[w] = v;
+                        }
+                    }
+                    ppp = set64(ppp, S, lane);
+                }
+            }
+            __syncwarp();
+        }
+        if ((ji & 31) != 0) {
+            const int w = ji >> 5;
+            tb[w * 32 + lane] = cur;
+            tba[w * 32 + lane] = (uint8_t)anc;
+        }
+
+        // ---- winner: least (metric, slot) among CRC-passing paths (scl.py:177-191) ----
+        const bool act = pl < P;
+        const bool ok = act && use_crc && syn == a.code.crc_offset;
+        const uint32_t okM = (__ballot_sync(FULL, ok) >> gbase) & gmask_lo;
+        const bool cnd = okM ? ok : act;
+        float key = cnd ? metric : INFINITY;
+        int who = cnd ? pl : L;
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1) {
+            const float k2 = __shfl_xor_sync(FULL, key, off);
+            const int w2 = __shfl_xor_sync(FULL, who, off);
+            if (k2 < key || (k2 == key && w2 < who)) {
+                key = k2;
+                who = w2;
+            }
+        }
+        __syncwarp();
+        if (grp_live && pl == 0) {
+            // traceback of the winner's decision windows
+            int l = gbase + who;
+            for (int w = W - 1; w >= 0; --w) {
+                wrow[grp * W + w] = tb[w * 32 + l];
+                l = gbase + (tba[w * 32 + l] - gbase);
+            }
+        }
+        __syncwarp();
+        if (grp_live) {
+            const uint32_t *row = wrow + grp * W;
+            const int NW = (N + 31) >> 5;
+            if (a.u_bits != nullptr)
+                for (int w = pl; w < NW; w += L) {
+                    int rank = 0;
+                    for (int z = 0; z < w; ++z)
+                        rank += 32 - __popc(__ldg(frzg + z));
+                    const uint32_t fw = __ldg(frzg + w);
+                    uint32_t v = 0;
+                    for (int q = 0; q < 32 && 32 * w + q < N; ++q)
+                        if (!((fw >> q) & 1u)) {
+                            v |= ((row[rank >> 5] >> (rank & 31)) & 1u) << q;
+                            ++rank;
+                        }
+                    a.u_bits[(size_t)frame * NW + w] = v;
+                }
+            if (a.payload != nullptr) {
+                const int MW = (a.code.m + 31) >> 5;
+                for (int w = pl; w < MW; w += L) {
+                    uint32_t v = row[w];
+                    if (32 * w + 32 > a.code.m)
+                        v &= (1u << (a.code.m & 31)) - 1u;
+                    a.payload[(size_t)frame * MW + w] = v;
+                }
+            }
+            if (pl == 0) {
+                if (a.metric != nullptr)
+                    a.metric[frame] = key;
+                if (a.crc_ok != nullptr)
+                    a.crc_ok[frame] = okM != 0;
+                if (a.sel != nullptr)
+                    a.sel[frame] = okM != 0;
+                if (a.t_done != nullptr)
+                    a.t_done[frame] = globaltimer();
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------- launchers --
+
+template <int L, bool FEX, int NV>
+inline int launch_scl3_t(const SclArgs &a, int wpc, int max_warps, cudaStream_t s)
+{
+    auto kern = k_scl3<L, FEX, NV>;
+    const size_t per_warp = (size_t)a.warp_words * 4;
+    const size_t smem_cap = 227 * 1024;
+    if (per_warp > smem_cap)
+        return PC_ERR_UNSUPPORTED;
+    while (wpc > 1 && (size_t)wpc * per_warp > smem_cap)
+        --wpc;
+    const size_t smem = (size_t)wpc * per_warp;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return PC_ERR_CUDA;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpc, smem) != cudaSuccess || per_sm < 1)
+        return PC_ERR_UNSUPPORTED;
+    long long grid = (long long)sms * per_sm;
+    const long long need = ((long long)max_warps + wpc - 1) / wpc;
+    if (grid > need)
+        grid = need;
+    if (grid < 1)
+        grid = 1;
+    kern<<<(int)grid, 32 * wpc, smem, s>>>(a);
+    return cudaGetLastError() == cudaSuccess ? PC_OK : PC_ERR_CUDA;
+}
+
+template <int L, bool FEX>
+inline int launch_scl3_nv(const SclArgs &a, int wpc, int max_warps, cudaStream_t s)
+{
+    switch (a.nv) {
+    case 0: return launch_scl3_t<L, FEX, 0>(a, wpc, max_warps, s);
+    case 1: return launch_scl3_t<L, FEX, 1>(a, wpc, max_warps, s);
+    case 2: return launch_scl3_t<L, FEX, 2>(a, wpc, max_warps, s);
+    case 3: return launch_scl3_t<L, FEX, 3>(a, wpc, max_warps, s);
+    case 4: return launch_scl3_t<L, FEX, 4>(a, wpc, max_warps, s);
+    default: return PC_ERR_UNSUPPORTED;
+    }
+}
+
+// One translation unit per list size (scl3_l*.cu) instantiates this, so the
+// 60 kernel variants compile in parallel.
+template <int L>
+int launch_scl3_for(const SclArgs &a, int wpc, int max_warps, cudaStream_t s)
+{
+    return a.f_exact ? launch_scl3_nv<L, true>(a, wpc, max_warps, s) : launch_scl3_nv<L, false>(a, wpc, max_warps, s);
+}
+
+} // namespace pc

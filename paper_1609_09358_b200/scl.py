@@ -54,7 +54,7 @@ class SclConfig:
         if not 0.0 <= self.da_threshold <= 1.0:
             raise ValueError("decision-aid threshold must lie in [0, 1]")
 
-    def native(self, virtual_levels: int | None = None, warps_per_cta: int = 0) -> nat.PcSclCfg:
+    def native(self, virtual_levels: int | None = None, warps_per_cta: int = 0, kernel: int | None = None) -> nat.PcSclCfg:
         if self.list_size > 32 or self.list_size & (self.list_size - 1):
             raise ValueError(
                 f"the device list decoder supports L in {{1, 2, 4, 8, 16, 32}}, got {self.list_size}"
@@ -66,6 +66,7 @@ class SclConfig:
             int(self.selector == "bitonic"),
             nat.env_int("PC_SCL_NV", -1) if virtual_levels is None else virtual_levels,
             warps_per_cta or nat.env_int("PC_SCL_WPC", 1),
+            nat.env_int("PC_SCL_KERNEL", 0) if kernel is None else kernel,
         )
 
 
