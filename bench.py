@@ -40,6 +40,7 @@ METRIC = "decoded info Gbit/s, hybrid BP+SCL N=1024 L=32, vs Eb/N0; p50 frame la
 EBNO = (1.0, 1.5, 2.0, 2.5, 3.0, 3.5, 4.0)
 N, K, LIST, IMAX = 1024, 512, 32, 50
 SEED = 20240917
+MUFU_PER_G = 3.5  # bp_pe2: 3 EX2 + 4 LG2 per processing element (2 exact g)
 WORKLOAD = "hybrid BP->SCL N=1024 K=512 (496 payload + CRC-16) L=32 i_max=50, Eb/N0 1-4 dB step 0.5"
 
 
@@ -248,7 +249,7 @@ def run_gpu(args):
     except Exception:
         pass
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak = sms * 16 * peak_mhz * 1e6 / 4 / 1e9  # MUFU ops/s / 4 MUFU per exact g, in Gg/s
+    peak = sms * 16 * peak_mhz * 1e6 / MUFU_PER_G / 1e9  # MUFU ops/s / MUFU per exact g, in Gg/s
     traffic = None
     prof = ROOT / "profiles" / "bp_kernel_ncu.json"
     if prof.exists():
@@ -260,8 +261,8 @@ def run_gpu(args):
         "bound": "xu", "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
         "traffic": traffic, "kernel": "k_bp2<10,256,0> (register/shuffle BP, TPF=256)",
         "note": "exact-g node updates/s of K1 vs the MUFU (XU) pipe bound: 148 SM x 16 MUFU/clk x sm_max_mhz / "
-                "4 MUFU per g; HBM is <1% (4.2 KB/frame)",
-        "peak_at_measured_clock": (sms * 16 * ck["sm_mhz"] * 1e6 / 4 / 1e9) if ck.get("sm_mhz") else None,
+                "3.5 MUFU per g (3 EX2 + 4 LG2 per PE); HBM is <1% (4.2 KB/frame)",
+        "peak_at_measured_clock": (sms * 16 * ck["sm_mhz"] * 1e6 / MUFU_PER_G / 1e9) if ck.get("sm_mhz") else None,
         # K1's own HBM traffic: read the LLRs, write payload + iters + flag + stamp per frame
         "hbm_gbs": len(EBNO) * B * (4 * N + 4 * MW + 4 + 1 + 8) / (bp_ms_step * 1e-3) / 1e9,
         "bp_share_of_step": bp_ms_step / (max_ms / args.steps),
@@ -345,7 +346,7 @@ def _xu_peak_gg(torch, dev):
     except Exception:
         pass
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    return sms * 16 * peak_mhz * 1e6 / 4 / 1e9
+    return sms * 16 * peak_mhz * 1e6 / MUFU_PER_G / 1e9
 
 
 def run_c4(args):
@@ -477,7 +478,7 @@ def run_c4(args):
                        "ber": float(errs_h[p, 0]) / (B * m)} for p, eb in enumerate(pts)],
             "roofline": {"bound": "xu", "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
                          "traffic": None, "kernel": "k_bp2<12,1024,0> (register/shuffle BP, 1024 threads/frame)",
-                         "note": "exact-g node updates/s (2nN per frame-iteration) vs 148 SM x 16 MUFU/clk / 4"},
+                         "note": "exact-g node updates/s (2nN per frame-iteration) vs 148 SM x 16 MUFU/clk / 3.5 MUFU per g"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "Gbit/s", "h2d_bytes_per_step": B * n4 * 4 * len(pts),
                     "d2h_bytes_per_step": B * (MW * 4 + 1) * len(pts)},

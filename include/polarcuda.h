@@ -61,7 +61,8 @@ typedef struct pc_code {
     const uint32_t *da_bits;     /* [ceil(N/32)] decision-aided positions or NULL  */
 } pc_code_t;
 
-/* BpConfig, bp.py:40-57.  g_mode 0 = exact, 1 = min; stop_mode 0 = crc,
+/* BpConfig, bp.py:40-57.  g_mode 0 = exact, 1 = min, 2 = exact evaluated per g
+ * (4 MUFU, the pre-exponential-domain form; N = 1024/2048, parity studies); stop_mode 0 = crc,
  * 1 = reencode, 2 = none.  threads_per_frame 0 = library default.
  * kernel: 0 = auto (register/shuffle kernel when eligible), 1 = shared-memory
  * kernel, 2 = register/shuffle kernel (N = 128..4096, crc/none stop, no soft_x;

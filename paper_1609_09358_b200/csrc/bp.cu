@@ -43,13 +43,10 @@ __device__ __forceinline__ void bp_pe(int j, int p, const float *__restrict__ Rp
         r2 = Rprev[i2];
     }
     const float l1 = Lj[i1], l2 = Lj[i2];
-    if (RSWEEP) {
-        o1 = bp_g<GMODE>(av, l2 + r2, lim);
-        o2 = clampf(bp_g<GMODE>(av, l1, lim) + r2, lim);
-    } else {
-        o1 = bp_g<GMODE>(l1, l2 + r2, lim);
-        o2 = clampf(bp_g<GMODE>(av, l1, lim) + l2, lim);
-    }
+    if (RSWEEP)
+        bp_pe2<GMODE>(av, l2 + r2, l1, r2, lim, o1, o2);
+    else
+        bp_pe2<GMODE>(l1, l2 + r2, av, l2, lim, o1, o2);
 }
 
 template <int LOGN>
@@ -266,8 +263,10 @@ __global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float lim)
             const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
             const float av = R[(j - 1) * N + i1], r2 = R[(j - 1) * N + i2];
             const float l1 = L[j * N + i1], l2 = L[j * N + i2];
-            R[j * N + i1] = bp_g<GMODE>(av, l2 + r2, lim);
-            R[j * N + i2] = clampf(bp_g<GMODE>(av, l1, lim) + r2, lim);
+            float o1, o2;
+            bp_pe2<GMODE>(av, l2 + r2, l1, r2, lim, o1, o2);
+            R[j * N + i1] = o1;
+            R[j * N + i2] = o2;
         }
         __syncthreads();
     }
@@ -277,8 +276,10 @@ __global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float lim)
             const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
             const float av = R[(j - 1) * N + i1], r2 = R[(j - 1) * N + i2];
             const float l1 = L[j * N + i1], l2 = L[j * N + i2];
-            L[(j - 1) * N + i1] = bp_g<GMODE>(l1, l2 + r2, lim);
-            L[(j - 1) * N + i2] = clampf(bp_g<GMODE>(av, l1, lim) + l2, lim);
+            float o1, o2;
+            bp_pe2<GMODE>(l1, l2 + r2, av, l2, lim, o1, o2);
+            L[(j - 1) * N + i1] = o1;
+            L[(j - 1) * N + i2] = o2;
         }
         __syncthreads();
     }
@@ -355,6 +356,8 @@ int launch_bp_decode(const BpArgs &a, int g_mode, int tpf, int kernel, cudaStrea
 {
     if (a.B == 0)
         return PC_OK;
+    if (g_mode == 2)
+        return launch_bp2(a, g_mode, tpf, s);
     if (kernel == 2 && !bp2_eligible(a, tpf))
         return PC_ERR_UNSUPPORTED;
     if (kernel != 1 && bp2_eligible(a, tpf))

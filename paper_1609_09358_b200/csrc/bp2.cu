@@ -108,8 +108,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                     continue;
                 const int r2 = r1 + h;
                 const float av = RGET(j - 1, r1), r2v = RGET(j - 1, r2), l1 = LGET(j, r1), l2 = LGET(j, r2);
-                Rr[j - 1][r1] = bp_g<GMODE>(av, l2 + r2v, lim);
-                Rr[j - 1][r2] = clampf(bp_g<GMODE>(av, l1, lim) + r2v, lim);
+                bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, Rr[j - 1][r1], Rr[j - 1][r2]);
             }
         }
 #pragma unroll
@@ -118,19 +117,32 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 break; // R[n] is not read by the sweeps
             const int msk = 1 << (j - 1 - B);
             const bool hi = lane & msk;
+            // Lane pair (lo = node i1, hi = node i2): the lo lane computes both outputs
+            // of nodes 0..Q/2-1, the hi lane those of nodes Q/2..Q-1, so the shared
+            // operand's exponential is evaluated once per PE (bp_pe2).
+            float Rn[Q];
+#pragma unroll
+            for (int k = 0; k < Q / 2; ++k) {
+                const float Rk = RGET(j - 1, k), Rh = RGET(j - 1, k + Q / 2);
+                const float Lk = LGET(j, k), Lh = LGET(j, k + Q / 2);
+                // send the partner the node it owns, keep mine (k on the lo lane, k + Q/2 on hi)
+                const float pr = __shfl_xor_sync(0xffffffffu, hi ? Rk : Rh, msk);
+                const float pl = __shfl_xor_sync(0xffffffffu, hi ? Lk : Lh, msk);
+                const float myR = hi ? Rh : Rk, myL = hi ? Lh : Lk;
+                // (a, r2, l1, l2) of the PE at my node
+                const float av = hi ? pr : myR, r2v = hi ? myR : pr, l1 = hi ? pl : myL, l2 = hi ? myL : pl;
+                float o1, o2;
+                bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                const float back = __shfl_xor_sync(0xffffffffu, hi ? o1 : o2, msk); // my output the partner computed
+                Rn[k] = hi ? back : o1;
+                Rn[k + Q / 2] = hi ? o2 : back;
+            }
 #pragma unroll
             for (int r = 0; r < Q; ++r) {
-                const float myR = RGET(j - 1, r), myL = LGET(j, r);
-                const float xo = __shfl_xor_sync(0xffffffffu, myR, msk);
-                const float yo = __shfl_xor_sync(0xffffffffu, myL, msk);
-                // i1 lane: g(a, l2 + r2) = g(myR, yo + xo); i2 lane: g(a, l1) + r2 = g(xo, yo) + myR
-                float o = bp_g<GMODE>(hi ? xo : myR, hi ? yo : yo + xo, lim);
-                if (hi)
-                    o = clampf(o + myR, lim);
                 if (j <= NREG)
-                    Rr[j - 1][r] = o;
+                    Rr[j - 1][r] = Rn[r];
                 else
-                    Rs[(j - BW) * N + base + r] = o;
+                    Rs[(j - BW) * N + base + r] = Rn[r];
             }
         }
         __syncthreads();
@@ -145,8 +157,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 const int p = tid + q * TPF;
                 const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
                 const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
-                Rd[i1] = bp_g<GMODE>(av, l2 + r2v, lim);
-                Rd[i2] = clampf(bp_g<GMODE>(av, l1, lim) + r2v, lim);
+                float o1, o2;
+                bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                Rd[i1] = o1;
+                Rd[i2] = o2;
             }
             __syncthreads();
         }
@@ -162,8 +176,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 const int p = tid + q * TPF;
                 const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
                 const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
-                Ld[i1] = bp_g<GMODE>(l1, l2 + r2v, lim);
-                Ld[i2] = clampf(bp_g<GMODE>(av, l1, lim) + l2, lim);
+                float o1, o2;
+                bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                Ld[i1] = o1;
+                Ld[i2] = o2;
             }
             __syncthreads();
         }
@@ -171,17 +187,26 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
         for (int j = BW; j >= B + 1; --j) {
             const int msk = 1 << (j - 1 - B);
             const bool hi = lane & msk;
+            float Ln[Q];
 #pragma unroll
-            for (int r = 0; r < Q; ++r) {
-                const float myR = RGET(j - 1, r), myL = LGET(j, r);
-                const float xo = __shfl_xor_sync(0xffffffffu, myR, msk);
-                const float yo = __shfl_xor_sync(0xffffffffu, myL, msk);
-                // i1 lane: g(l1, l2 + r2) = g(myL, yo + xo); i2 lane: g(a, l1) + l2 = g(xo, yo) + myL
-                float o = bp_g<GMODE>(hi ? xo : myL, hi ? yo : yo + xo, lim);
-                if (hi)
-                    o = clampf(o + myL, lim);
-                Lr[j - 2][r] = o; // j - 1 >= B >= 1 is a register stage
+            for (int k = 0; k < Q / 2; ++k) {
+                const float Rk = RGET(j - 1, k), Rh = RGET(j - 1, k + Q / 2);
+                const float Lk = LGET(j, k), Lh = LGET(j, k + Q / 2);
+                // send the partner the node it owns, keep mine (k on the lo lane, k + Q/2 on hi)
+                const float pr = __shfl_xor_sync(0xffffffffu, hi ? Rk : Rh, msk);
+                const float pl = __shfl_xor_sync(0xffffffffu, hi ? Lk : Lh, msk);
+                const float myR = hi ? Rh : Rk, myL = hi ? Lh : Lk;
+                // (a, r2, l1, l2) of the PE at my node
+                const float av = hi ? pr : myR, r2v = hi ? myR : pr, l1 = hi ? pl : myL, l2 = hi ? myL : pl;
+                float o1, o2;
+                bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                const float back = __shfl_xor_sync(0xffffffffu, hi ? o1 : o2, msk); // my output the partner computed
+                Ln[k] = hi ? back : o1;
+                Ln[k + Q / 2] = hi ? o2 : back;
             }
+#pragma unroll
+            for (int r = 0; r < Q; ++r)
+                Lr[j - 2][r] = Ln[r]; // j - 1 >= B >= 1 is a register stage
         }
 #pragma unroll
         for (int j = B; j >= 1; --j) {
@@ -192,8 +217,8 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                     continue;
                 const int r2 = r1 + h;
                 const float av = RGET(j - 1, r1), r2v = RGET(j - 1, r2), l1 = LGET(j, r1), l2 = LGET(j, r2);
-                const float o1 = bp_g<GMODE>(l1, l2 + r2v, lim);
-                const float o2 = clampf(bp_g<GMODE>(av, l1, lim) + l2, lim);
+                float o1, o2;
+                bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
                 if (j > 1) {
                     Lr[j - 2][r1] = o1;
                     Lr[j - 2][r2] = o2;
@@ -321,6 +346,13 @@ int launch_bp2(const BpArgs &a, int g_mode, int tpf, cudaStream_t s)
     if (a.B == 0)
         return PC_OK;
     const int n = a.code.n;
+    if (g_mode == 2) { // exact g, per-g form (parity studies)
+        switch (n) {
+        case 10: return launch_bp2_n<10, 2>(a, tpf, s);
+        case 11: return launch_bp2_n<11, 2>(a, tpf, s);
+        }
+        return PC_ERR_UNSUPPORTED;
+    }
     if (g_mode == 0) {
         switch (n) {
         case 7: return launch_bp2_n<7, 0>(a, tpf, s);

@@ -26,4 +26,46 @@ __device__ __forceinline__ float bp_g(float a, float b, float lim)
     return __uint_as_float(__float_as_uint(mag) ^ sgn);
 }
 
+// Both node updates of one processing element share an operand x (bp.py:145-158):
+//   R sweep  x = a,  y1 = l2 + r2, y2 = l1, add = r2:  o1 = g(a, l2 + r2),  o2 = clip(g(a, l1) + r2)
+//   L sweep  x = l1, y1 = l2 + r2, y2 = a,  add = l2:  o1 = g(l1, l2 + r2), o2 = clip(g(a, l1) + l2)
+// Exact g in the exponential domain, p = e^-|v| in (0, 1]:
+//   |g(x, y)| = ln(1 + px py) - ln(px + py)            (= logaddexp(0, x+y) - logaddexp(x, y), bp.py:95)
+// so a PE costs 3 EX2 + 4 LG2 on the MUFU pipe (px shared) instead of 8.  The
+// magnitude is clamped to [lb, m], m = min(|x|, |y|).  The difference of two
+// fp32 logs has an absolute error near 1e-7 and would flush tiny exact values
+// (|g| ~ m tanh(M/2) for m -> 0) to 0; lb = min(m, 2^-10) (2 - X) / 2, X = 1 + px py,
+// keeps their sign and first-order magnitude (an
+// absolute deviation below 2^-20 from the exact value; tools/bp_formula_study.py).
+template <int GMODE>
+__device__ __forceinline__ void bp_pe2(float x, float y1, float y2, float add, float lim, float &o1, float &o2)
+{
+    if (GMODE == 2) {
+        o1 = bp_g<0>(x, y1, lim);
+        o2 = clampf(bp_g<0>(x, y2, lim) + add, lim);
+        return;
+    }
+    const float ax = fabsf(x), a1 = fabsf(y1), a2 = fabsf(y2);
+    float m1, m2;
+    if (GMODE == 0) {
+        const float px = ex2_approx(-ax * PC_LOG2E);
+        const float p1 = ex2_approx(-a1 * PC_LOG2E);
+        const float p2 = ex2_approx(-a2 * PC_LOG2E);
+        const float X1 = fmaf(px, p1, 1.0f), X2 = fmaf(px, p2, 1.0f);
+        m1 = PC_LN2 * (lg2_approx(X1) - lg2_approx(px + p1));
+        m2 = PC_LN2 * (lg2_approx(X2) - lg2_approx(px + p2));
+        const float n1 = fminf(ax, a1), n2 = fminf(ax, a2);
+        const float lb1 = fminf(n1, 0.0009765625f) * fmaf(-0.5f, X1, 1.0f);
+        const float lb2 = fminf(n2, 0.0009765625f) * fmaf(-0.5f, X2, 1.0f);
+        m1 = fminf(fmaxf(m1, lb1), n1);
+        m2 = fminf(fmaxf(m2, lb2), n2);
+    } else {
+        m1 = (x == 0.0f || y1 == 0.0f) ? 0.0f : fminf(ax, a1);
+        m2 = (x == 0.0f || y2 == 0.0f) ? 0.0f : fminf(ax, a2);
+    }
+    o1 = __uint_as_float(__float_as_uint(m1) ^ ((__float_as_uint(x) ^ __float_as_uint(y1)) & 0x80000000u));
+    const float g2 = __uint_as_float(__float_as_uint(m2) ^ ((__float_as_uint(x) ^ __float_as_uint(y2)) & 0x80000000u));
+    o2 = clampf(g2 + add, lim);
+}
+
 } // namespace pc
