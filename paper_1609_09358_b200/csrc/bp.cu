@@ -79,14 +79,15 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int f = blockIdx.x;
-    const float lim = a.llr_max;
+    constexpr float KIN = bp_unit_in<GMODE>(), KOUT = bp_unit_out<GMODE>();
+    const float lim = a.llr_max * KIN; // messages in the kernel's units (bp_math.cuh)
 
     for (int w = tid; w < NW; w += TPF)
         frz[w] = a.code.frozen_bits[w];
     const float *x = a.llr + (size_t)f * N;
     float *Lch = Ls + (LOGN - 1) * N;
     for (int i = tid; i < N; i += TPF)
-        Lch[i] = clampf(__ldg(x + i), lim);
+        Lch[i] = clampf(__ldg(x + i) * KIN, lim);
     for (int i = tid; i < (LOGN - 1) * N; i += TPF) {
         Rs[i] = 0.0f;
         Ls[i] = 0.0f;
@@ -203,7 +204,8 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
     for (int q = 0; q < PPT; ++q) {
         const int p = tid + q * TPF;
         if (a.soft_u != nullptr)
-            *reinterpret_cast<float2 *>(a.soft_u + (size_t)f * N + 2 * p) = make_float2(su[q][0], su[q][1]);
+            *reinterpret_cast<float2 *>(a.soft_u + (size_t)f * N + 2 * p) =
+                make_float2(su[q][0] * KOUT, su[q][1] * KOUT);
         ub[2 * p] = su[q][0] < 0.0f;
         ub[2 * p + 1] = su[q][1] < 0.0f;
     }
@@ -215,8 +217,8 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
             bp_pe<GMODE, true>(LOGN, p, Rp, Lch, frz, lim, o1, o2, av, r2);
             int i1, i2;
             pe_nodes<LOGN>(LOGN, p, i1, i2);
-            a.soft_x[(size_t)f * N + i1] = Lch[i1] + o1;
-            a.soft_x[(size_t)f * N + i2] = Lch[i2] + o2;
+            a.soft_x[(size_t)f * N + i1] = (Lch[i1] + o1) * KOUT;
+            a.soft_x[(size_t)f * N + i2] = (Lch[i2] + o2) * KOUT;
         }
     }
     __syncthreads();
@@ -247,13 +249,14 @@ __global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float lim)
     extern __shared__ __align__(16) float st[];
     const int N = 1 << n;
     const size_t base = (size_t)blockIdx.x * (n + 1) * N;
+    constexpr float KIN = bp_unit_in<GMODE>(), KOUT = bp_unit_out<GMODE>();
     float *L = SMEM ? st : l_msgs + base;
     float *R = SMEM ? st + (size_t)(n + 1) * N : r_msgs + base;
-    if (SMEM) {
-        for (int i = threadIdx.x; i < (n + 1) * N; i += blockDim.x) {
-            L[i] = l_msgs[base + i];
-            R[i] = r_msgs[base + i];
-        }
+    const float lim_out = lim;
+    lim *= KIN;
+    for (int i = threadIdx.x; i < (n + 1) * N; i += blockDim.x) { // into the kernel's message units
+        L[i] = l_msgs[base + i] * KIN;
+        R[i] = r_msgs[base + i] * KIN;
     }
     __syncthreads();
     const int NPE = N / 2;
@@ -283,11 +286,9 @@ __global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float lim)
         }
         __syncthreads();
     }
-    if (SMEM) {
-        for (int i = threadIdx.x; i < (n + 1) * N; i += blockDim.x) {
-            l_msgs[base + i] = L[i];
-            r_msgs[base + i] = R[i];
-        }
+    for (int i = threadIdx.x; i < (n + 1) * N; i += blockDim.x) {
+        l_msgs[base + i] = clampf(L[i] * KOUT, lim_out);
+        r_msgs[base + i] = clampf(R[i] * KOUT, lim_out);
     }
 }
 

@@ -55,7 +55,8 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int f = blockIdx.x;
-    const float lim = a.llr_max;
+    constexpr float KIN = bp_unit_in<GMODE>(), KOUT = bp_unit_out<GMODE>();
+    const float lim = a.llr_max * KIN; // messages in the kernel's units (bp_math.cuh)
     const int base = warp * 32 * Q + lane * Q;
 
     for (int w = tid; w < NW; w += TPF)
@@ -64,8 +65,8 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
     float *Lch = Ls + (NSL - 1) * N;
     for (int i = 4 * tid; i < N; i += 4 * TPF) {
         const float4 v = __ldg(reinterpret_cast<const float4 *>(x + i));
-        *reinterpret_cast<float4 *>(Lch + i) = make_float4(clampf(v.x, lim), clampf(v.y, lim), clampf(v.z, lim),
-                                                          clampf(v.w, lim));
+        *reinterpret_cast<float4 *>(Lch + i) = make_float4(clampf(v.x * KIN, lim), clampf(v.y * KIN, lim),
+                                                          clampf(v.z * KIN, lim), clampf(v.w * KIN, lim));
     }
     for (int i = tid; i < NSR * N; i += TPF)
         Rs[i] = 0.0f;
@@ -261,7 +262,8 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
     if (a.soft_u != nullptr) {
 #pragma unroll
         for (int r = 0; r < Q; r += 2)
-            *reinterpret_cast<float2 *>(a.soft_u + (size_t)f * N + base + r) = make_float2(su[r], su[r + 1]);
+            *reinterpret_cast<float2 *>(a.soft_u + (size_t)f * N + base + r) =
+                make_float2(su[r] * KOUT, su[r + 1] * KOUT);
     }
     __syncthreads();
     if (a.u_bits != nullptr)

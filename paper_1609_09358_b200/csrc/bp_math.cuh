@@ -32,11 +32,20 @@ __device__ __forceinline__ float bp_g(float a, float b, float lim)
 // Exact g in the exponential domain, p = e^-|v| in (0, 1]:
 //   |g(x, y)| = ln(1 + px py) - ln(px + py)            (= logaddexp(0, x+y) - logaddexp(x, y), bp.py:95)
 // so a PE costs 3 EX2 + 4 LG2 on the MUFU pipe (px shared) instead of 8.  The
-// magnitude is clamped to [lb, m], m = min(|x|, |y|).  The difference of two
+// magnitude is floored at lb (m = min(|x|, |y|), M = max).  The difference of two
 // fp32 logs has an absolute error near 1e-7 and would flush tiny exact values
 // (|g| ~ m tanh(M/2) for m -> 0) to 0; lb = min(m, 2^-10) (2 - X) / 2, X = 1 + px py,
 // keeps their sign and first-order magnitude (an
 // absolute deviation below 2^-20 from the exact value; tools/bp_formula_study.py).
+// Message units: with GMODE 0 the kernels keep every message in log2 units
+// (LLR * log2 e; see bp_unit_in/out), so EX2 and LG2 need no scaling multiply.
+// The min-sum and per-g modes use natural units (min-sum stays bit-identical
+// to an fp32 restatement of the reference).
+template <int GMODE>
+__host__ __device__ constexpr float bp_unit_in() { return GMODE == 0 ? PC_LOG2E : 1.0f; }
+template <int GMODE>
+__host__ __device__ constexpr float bp_unit_out() { return GMODE == 0 ? PC_LN2 : 1.0f; }
+
 template <int GMODE>
 __device__ __forceinline__ void bp_pe2(float x, float y1, float y2, float add, float lim, float &o1, float &o2)
 {
@@ -47,18 +56,19 @@ __device__ __forceinline__ void bp_pe2(float x, float y1, float y2, float add, f
     }
     const float ax = fabsf(x), a1 = fabsf(y1), a2 = fabsf(y2);
     float m1, m2;
-    if (GMODE == 0) {
-        const float px = ex2_approx(-ax * PC_LOG2E);
-        const float p1 = ex2_approx(-a1 * PC_LOG2E);
-        const float p2 = ex2_approx(-a2 * PC_LOG2E);
+    if (GMODE == 0) { // log2 units: p = 2^-|v'|, |g'| = lg2(1 + px py) - lg2(px + py)
+        const float px = ex2_approx(-ax);
+        const float p1 = ex2_approx(-a1);
+        const float p2 = ex2_approx(-a2);
         const float X1 = fmaf(px, p1, 1.0f), X2 = fmaf(px, p2, 1.0f);
-        m1 = PC_LN2 * (lg2_approx(X1) - lg2_approx(px + p1));
-        m2 = PC_LN2 * (lg2_approx(X2) - lg2_approx(px + p2));
-        const float n1 = fminf(ax, a1), n2 = fminf(ax, a2);
-        const float lb1 = fminf(n1, 0.0009765625f) * fmaf(-0.5f, X1, 1.0f);
-        const float lb2 = fminf(n2, 0.0009765625f) * fmaf(-0.5f, X2, 1.0f);
-        m1 = fminf(fmaxf(m1, lb1), n1);
-        m2 = fminf(fmaxf(m2, lb2), n2);
+        m1 = lg2_approx(X1) - lg2_approx(px + p1);
+        m2 = lg2_approx(X2) - lg2_approx(px + p2);
+        // (no upper clamp at min(|x|, |y|): the computed value exceeds it by rounding
+        // noise only, and every message is clipped or feeds a clipped one)
+        const float lb1 = fminf(fminf(ax, a1), 0.0009765625f) * fmaf(-0.5f, X1, 1.0f);
+        const float lb2 = fminf(fminf(ax, a2), 0.0009765625f) * fmaf(-0.5f, X2, 1.0f);
+        m1 = fmaxf(m1, lb1);
+        m2 = fmaxf(m2, lb2);
     } else {
         m1 = (x == 0.0f || y1 == 0.0f) ? 0.0f : fminf(ax, a1);
         m2 = (x == 0.0f || y2 == 0.0f) ? 0.0f : fminf(ax, a2);
