@@ -104,6 +104,19 @@ __device__ __forceinline__ int gmin_i(int v)
     }
 }
 
+template <int L>
+__device__ __forceinline__ int gsum_i(int v)
+{
+    if constexpr (L == 32) {
+        return __reduce_add_sync(0xffffffffu, v);
+    } else {
+#pragma unroll
+        for (int off = 1; off < L; off <<= 1)
+            v += __shfl_xor_sync(0xffffffffu, v, off);
+        return v;
+    }
+}
+
 } // namespace s3
 
 template <int L, bool FEX, int NV>
@@ -331,23 +344,44 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                                         inB = true;
                                 }
                             } else {
-                                // rank inside U by the exact (metric, index) key
+                                // rank inside U by (metric, index): strict metric ranks first,
+                                // the exact key only when U holds tied metrics (rank sum check)
                                 const uint32_t below = (1u << pl) - 1u;
                                 const int nu = h + l;
-                                unsigned long long *uk = reinterpret_cast<unsigned long long *>(cg);
-                                const unsigned long long kg = ((unsigned long long)gk << 8) | (unsigned)gi;
-                                const unsigned long long kb = ((unsigned long long)bk << 8) | (unsigned)bi;
-                                if (hiG)
-                                    uk[__popc(gb & below)] = kg;
-                                if (loB)
-                                    uk[h + __popc(bb & below)] = kb;
+                                float *um = cg;                                 // U metrics
+                                int *ui = reinterpret_cast<int *>(cg + 2 * L);  // U candidate indices
+                                const int qg = __popc(gb & below), qb = h + __popc(bb & below);
+                                if (hiG) {
+                                    um[qg] = gv;
+                                    ui[qg] = gi;
+                                }
+                                if (loB) {
+                                    um[qb] = bv;
+                                    ui[qb] = bi;
+                                }
+                                if (nu & 1)
+                                    um[nu] = INFINITY; // pad to pairs
                                 __syncwarp();
                                 int rg = 0, rb = 0;
                                 const int numax = __reduce_max_sync(FULL, nu);
-                                for (int q = 0; q < numax; ++q) {
-                                    const unsigned long long v = q < nu ? uk[q] : ~0ull;
-                                    rg += v < kg;
-                                    rb += v < kb;
+                                for (int q = 0; q < numax; q += 2) {
+                                    const float2 v = *reinterpret_cast<const float2 *>(um + q);
+                                    const bool l0 = q < nu, l1v = q + 1 < nu;
+                                    rg += (l0 && v.x < gv) + (l1v && v.y < gv);
+                                    rb += (l0 && v.x < bv) + (l1v && v.y < bv);
+                                }
+                                // no ties inside U <=> the strict ranks of its nu elements sum to nu(nu-1)/2
+                                const int rsum = gsum_i<L>((hiG ? rg : 0) + (loB ? rb : 0));
+                                if (__any_sync(FULL, rsum != nu * (nu - 1) / 2)) {
+                                    rg = 0;
+                                    rb = 0;
+                                    for (int q = 0; q < numax; ++q) {
+                                        const float v = um[q];
+                                        const int vi = ui[q];
+                                        const bool live = q < nu;
+                                        rg += live && (v < gv || (v == gv && vi < gi));
+                                        rb += live && (v < bv || (v == bv && vi < bi));
+                                    }
                                 }
                                 if (hiG)
                                     inG = rg < h;
