@@ -135,7 +135,7 @@ int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32
     int nv = cfg->virtual_levels;
     if (cfg->kernel != 1 && scl3_eligible(a, L)) {
         if (nv < 0)
-            nv = code->n >= 12 ? 4 : (code->n >= 10 ? 3 : (code->n >= 8 ? 2 : 0));
+            nv = code->n >= 10 ? 3 : (code->n >= 8 ? 2 : 0); // measured best at N = 1024..4096
         const int rc3 = scl3_prepare(a, L, nv);
         if (rc3)
             return rc3;

@@ -264,11 +264,11 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
             const uint32_t daw = damg != nullptr ? (__ldg(damg + (i0 >> 5)) >> (i0 & 31)) & ((1u << BL) - 1u) : 0u;
 
             // ================= the block's leaves, registers only =================
-            static_assert(T == 3, "the leaf code below is written for 8-leaf blocks");
-            float l2[4], l1[2]; // levels 2 and 1 of the block (level 3 is x)
+            static_assert(T == 3 || T == 4, "the leaf code below is written for 8- or 16-leaf blocks");
+            float l3[8], l2[4], l1[2]; // levels 3 (T = 4 only), 2, 1 of the block; level T is x
             uint32_t psr = 0;   // partial sums of levels < T: level s at bits [2^s - 1, 2^(s+1) - 1)
             uint32_t betaT = 0; // the block's codeword (2^T bits) after its last leaf
-            // One copy of the leaf code for all 8 leaves (runtime j, warp-uniform
+            // One copy of the leaf code for all leaves (runtime j, warp-uniform
             // branches): an unrolled block overflows the instruction cache.
 #pragma unroll 1
             for (int j = 0; j < BL; ++j) {
@@ -281,14 +281,26 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                         l1[0] = scl_g(l2[0], l2[2], (psr >> 1) & 1u);
                         l1[1] = scl_g(l2[1], l2[3], (psr >> 2) & 1u);
                     } else {
+                        const float *L3 = (T == 3) ? x : l3;
                         if (j & 4) {
 #pragma unroll
                             for (int t = 0; t < 4; ++t)
-                                l2[t] = scl_g(x[t], x[t + 4], (psr >> (3 + t)) & 1u);
+                                l2[t] = scl_g(L3[t], L3[t + 4], (psr >> (3 + t)) & 1u);
                         } else {
+                            if constexpr (T == 4) {
+                                if (j & 8) {
+#pragma unroll
+                                    for (int t = 0; t < 8; ++t)
+                                        l3[t] = scl_g(x[t], x[t + 8], (psr >> (7 + t)) & 1u);
+                                } else {
+#pragma unroll
+                                    for (int t = 0; t < 8; ++t)
+                                        l3[t] = scl_f<FEX>(x[t], x[t + 8]);
+                                }
+                            }
 #pragma unroll
                             for (int t = 0; t < 4; ++t)
-                                l2[t] = scl_f<FEX>(x[t], x[t + 4]);
+                                l2[t] = scl_f<FEX>(L3[t], L3[t + 4]);
                         }
                         l1[0] = scl_f<FEX>(l2[0], l2[2]);
                         l1[1] = scl_f<FEX>(l2[1], l2[3]);
@@ -416,10 +428,15 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                         const float pc1 = __shfl_sync(FULL, c1, src);
                         // eager copy of the still-readable register levels: level s+1 while
                         // bit s of j is 0 (the reference's rule at _kernels.py:296-303)
-                        if ((j & 4) == 0) {
+                        if (((j >> (T - 1)) & 1) == 0) {
 #pragma unroll
                             for (int t = 0; t < BL; ++t)
                                 x[t] = __shfl_sync(FULL, x[t], src);
+                        }
+                        if (T == 4 && (j & 4) == 0) {
+#pragma unroll
+                            for (int t = 0; t < 8; ++t)
+                                l3[t] = __shfl_sync(FULL, l3[t], src);
                         }
                         if ((j & 2) == 0) {
 #pragma unroll
@@ -470,10 +487,19 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                         Fw = ((psr ^ Fw) & 1u) | (Fw << 1);
                         if (j & 2) {
                             Fw = (((psr >> 1) ^ Fw) & 3u) | (Fw << 2);
-                            if (j & 4)
-                                betaT = (((psr >> 3) ^ Fw) & 15u) | (Fw << 4);
-                            else
+                            if (j & 4) {
+                                Fw = (((psr >> 3) ^ Fw) & 15u) | (Fw << 4);
+                                if constexpr (T == 3) {
+                                    betaT = Fw;
+                                } else {
+                                    if (j & 8)
+                                        betaT = (((psr >> 7) ^ Fw) & 255u) | (Fw << 8);
+                                    else
+                                        psr = (psr & ~(255u << 7)) | (Fw << 7);
+                                }
+                            } else {
                                 psr = (psr & ~(15u << 3)) | (Fw << 3);
+                            }
                         } else {
                             psr = (psr & ~(3u << 1)) | (Fw << 1);
                         }

@@ -4,7 +4,10 @@
 
 namespace pc {
 namespace s3 {
-constexpr int T = 3;       // leaf-block level: 2^T leaves per block
+#ifndef PC_SCL3_T
+#define PC_SCL3_T 4
+#endif
+constexpr int T = PC_SCL3_T; // leaf-block level: 2^T leaves per block (3 or 4)
 constexpr int BL = 1 << T; // leaves per block
 // word offset of partial-sum level s (T <= s <= n-1) inside a slot
 __host__ __device__ __forceinline__ int pso(int s) { return s < 5 ? s - T : (5 - T) + (1 << (s - 5)) - 1; }
