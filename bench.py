@@ -275,13 +275,11 @@ def run_gpu(args):
         for p in range(len(EBNO)):
             host[p].copy_(llr[p])
         torch.cuda.synchronize()
-        for p in range(len(EBNO)):
-            dec.decode_host(host[p])
+        dec.decode_host_many(host)  # warm-up (allocates the double buffers)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            for p in range(len(EBNO)):
-                dec.decode_host(host[p])
+            dec.decode_host_many(host)  # H2D of point p+1 overlaps the decode of point p
         barrier()
         e2e_s = time.perf_counter() - t0
         e2e_val = world * bits_step * args.steps / max_over_ranks(e2e_s, device=dev) / 1e9
@@ -425,17 +423,37 @@ def run_c4(args):
     host = [torch.empty((B, n4), dtype=torch.float32, pin_memory=True) for _ in pts]
     for p in range(len(pts)):
         host[p].copy_(llr[p])
-    pay_h = torch.empty((B, MW), dtype=torch.int32, pin_memory=True)
-    conv_h = torch.empty(B, dtype=torch.uint8, pin_memory=True)
-    dbuf = torch.empty((B, n4), dtype=torch.float32, device=dev)
+    pay_h = [torch.empty((B, MW), dtype=torch.int32, pin_memory=True) for _ in pts]
+    conv_h = [torch.empty(B, dtype=torch.uint8, pin_memory=True) for _ in pts]
+    dbufs = [torch.empty((B, n4), dtype=torch.float32, device=dev) for _ in range(2)]
+    s_copy = torch.cuda.Stream(device=dev)
 
     def e2e_step():
+        # H2D of point p+1 on a copy stream overlaps the decode of point p
+        cur = torch.cuda.current_stream(dev)
+        h2d, done = [], []
+
+        def issue(i):
+            with torch.cuda.stream(s_copy):
+                if i >= 2:
+                    s_copy.wait_event(done[i - 2])
+                dbufs[i % 2].copy_(host[i], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(s_copy)
+                h2d.append(e)
+
+        issue(0)
         for p in range(len(pts)):
-            dbuf.copy_(host[p], non_blocking=True)
-            nat.check(lib.pc_bp_decode(dbuf.data_ptr(), B, dc.ref, ctypes.byref(cfg), None, pay.data_ptr(), None,
-                                       None, iters[p].data_ptr(), conv[p].data_ptr(), None, st), "pc_bp_decode")
-            pay_h.copy_(pay, non_blocking=True)
-            conv_h.copy_(conv[p], non_blocking=True)
+            if p + 1 < len(pts):
+                issue(p + 1)
+            cur.wait_event(h2d[p])
+            nat.check(lib.pc_bp_decode(dbufs[p % 2].data_ptr(), B, dc.ref, ctypes.byref(cfg), None, pay.data_ptr(),
+                                       None, None, iters[p].data_ptr(), conv[p].data_ptr(), None, st), "pc_bp_decode")
+            e = torch.cuda.Event()
+            e.record(cur)
+            done.append(e)
+            pay_h[p].copy_(pay, non_blocking=True)
+            conv_h[p].copy_(conv[p], non_blocking=True)
         torch.cuda.synchronize()
 
     e2e_step()

@@ -204,6 +204,57 @@ class HybridDecoder:
         torch.cuda.current_stream(self.device).synchronize()
         return self._pay_host[:B].numpy().view(np.uint32), self._conv_host[:B].numpy().astype(bool)
 
+    def decode_host_many(self, batches):
+        """End-to-end call over several HOST batches (pinned float32 [B_i, N]):
+        the H2D copy of batch i+1 runs on a copy stream while batch i decodes
+        (two device input buffers), each batch's payload words and converged
+        flags are read back right after its decode.  Returns a list of
+        (payload words uint32 [B_i, ceil(m/32)], converged bool [B_i]) numpy
+        arrays, in order.  Results equal ``decode_host`` per batch."""
+        torch = self.torch
+        dev = self.device
+        if not batches:
+            return []
+        for b in batches:
+            if b.shape[0] > self.capacity:
+                raise ValueError(f"batch of {b.shape[0]} frames exceeds capacity {self.capacity}")
+        N = self.code.N
+        if getattr(self, "_dbuf", None) is None or self._dbuf[0].shape[0] < self.capacity:
+            self._dbuf = [torch.empty((self.capacity, N), dtype=torch.float32, device=dev) for _ in range(2)]
+            self._s_copy = torch.cuda.Stream(device=dev)
+        cur = torch.cuda.current_stream(dev)
+        outs = []
+        h2d = [None] * len(batches)
+        done = [None] * len(batches)
+
+        def issue_h2d(i):
+            buf = self._dbuf[i % 2]
+            with torch.cuda.stream(self._s_copy):
+                if i >= 2:  # the buffer is free once batch i-2 has decoded
+                    self._s_copy.wait_event(done[i - 2])
+                buf[: batches[i].shape[0]].copy_(batches[i], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self._s_copy)
+            h2d[i] = ev
+
+        issue_h2d(0)
+        for i, b in enumerate(batches):
+            if i + 1 < len(batches):
+                issue_h2d(i + 1)
+            B = int(b.shape[0])
+            cur.wait_event(h2d[i])
+            self.run(self._dbuf[i % 2][:B], B)
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            done[i] = ev
+            pay = torch.empty((B, self.MW), dtype=torch.int32, pin_memory=True)
+            conv = torch.empty(B, dtype=torch.uint8, pin_memory=True)
+            pay.copy_(self.payload[:B], non_blocking=True)
+            conv.copy_(self.conv[:B], non_blocking=True)
+            outs.append((pay, conv))
+        cur.synchronize()
+        return [(p.numpy().view(np.uint32), c.numpy().astype(bool)) for p, c in outs]
+
     def _st(self, s) -> int:
         return int(s.cuda_stream)
 

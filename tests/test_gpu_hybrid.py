@@ -125,3 +125,22 @@ def test_validation():
         hybrid_decode_batch([FrameJob(0, np.zeros(32))], code, bp_batch_size=0)
     with pytest.raises(ValueError):
         hybrid_decode_batch([FrameJob(0, np.zeros(16))], CodeConfig(16, 8, crc=None))
+
+
+def test_host_buffer_pipeline_matches_device_run():
+    """decode_host_many (H2D of batch i+1 overlapping the decode of batch i)
+    returns exactly what run() produces batch by batch."""
+    import torch
+
+    code = CodeConfig(1024, 512, crc=16)
+    batches = []
+    for p, eb in enumerate((1.0, 2.0, 3.0)):
+        sigma = ebno_to_sigma(eb, code.rate)
+        llrs = np.array([make_frame(code, sigma, frame_rng(55, p, f))[1] for f in range(300 + 50 * p)])
+        batches.append(torch.from_numpy(llrs.astype(np.float32)).pin_memory())
+    dec = HybridDecoder(code, BpConfig(i_max=50), SclConfig(32), capacity=400, chunk=128)
+    got = dec.decode_host_many(batches)
+    for b, (pay, conv) in zip(batches, got):
+        dec.run(b.cuda(), b.shape[0]).sync()
+        r = dec.host_results()
+        assert np.array_equal(pay, r["payload"]) and np.array_equal(conv, r["converged"])
