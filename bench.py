@@ -231,6 +231,14 @@ def run_gpu(args):
         nat.check(lib.pc_count_errors(dec.payload.data_ptr(), msg[p].data_ptr(), B, m, errs[p].data_ptr(),
                                       nat.stream_handle()), "pc_count_errors")
     torch.cuda.synchronize()
+    if world > 1:  # whole-job statistics: sum the per-rank counters (off the timed path)
+        stats = torch.tensor([[iters_sum[p], round(gammas[p] * B)] for p in range(len(EBNO))], dtype=torch.int64,
+                             device=dev)
+        dist.all_reduce(stats)
+        dist.all_reduce(errs)
+        for p in range(len(EBNO)):
+            iters_sum[p] = int(stats[p, 0]) / world  # per-rank average keeps the per-GPU roofline arithmetic
+            gammas[p] = float(stats[p, 1]) / (B * world)
     errs_h = errs.cpu().numpy()
 
     max_ms = max_over_ranks(elapsed_ms, device=dev)
@@ -302,7 +310,8 @@ def run_gpu(args):
         ms = pt_ms[p] / args.steps
         sweep.append({"ebno_db": eb, "gbps": B * m / (ms * 1e-3) / 1e9 * world, "ms": ms, "gamma": gammas[p],
                       "mean_bp_iters": iters_sum[p] / B, "p50_latency_ms": lat_p50[p],
-                      "fer": float(errs_h[p, 1]) / B, "ber": float(errs_h[p, 0]) / (B * m), "frames": B * world})
+                      "fer": float(errs_h[p, 1]) / (B * world), "ber": float(errs_h[p, 0]) / (B * m * world),
+                      "frames": B * world})
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
