@@ -172,6 +172,8 @@ def main():
             cells = dict(zip(hdr, l.split(",")))
             rows.append({k: cells[k] for k in ("ebno_db", "frames", "bit_errors", "frame_errors", "gamma_bp_fer")})
         fx[p.stem] = dict(config=cfgline, rows=rows)
+        if p.stem == "no_timing":  # byte-identity target for the CLI (--no-timing)
+            fx[p.stem]["raw"] = p.read_text()
     (OUT / "golden_meta.json").write_text(json.dumps(dict(sets=meta, fixtures=fx), indent=1, sort_keys=True))
     print("wrote", OUT / "golden.npz", (OUT / "golden.npz").stat().st_size, "bytes")
 

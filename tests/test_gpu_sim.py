@@ -50,3 +50,17 @@ def test_sweep_reproduces_reference_fixture(golden_meta, name):
         assert rec.bit_errors == int(row["bit_errors"]), (rec, row)
         if row["gamma_bp_fer"]:
             assert abs(rec.gamma_bp_fer - float(row["gamma_bp_fer"])) <= 2.0 / rec.frames, (rec, row)
+
+
+def test_cli_no_timing_is_byte_identical_to_reference_fixture(golden_meta, tmp_path):
+    """The reference's --no-timing CSV (plot-tool fixture no_timing.csv, config
+    N=128 k=64 scl L=2, 2 and 3 dB, seed 14) reproduced byte for byte through
+    the CLI (reference cli.py:72-115, test_acceptance.py:311-331)."""
+    from paper_1609_09358_b200.cli import main
+
+    out = tmp_path / "sweep.csv"
+    rc = main(["--n", "128", "--k", "64", "--decoder", "scl", "--list-size", "2", "--ebno", "2:3:1",
+               "--seed", "14", "--min-frame-errors", "10", "--max-frames", "500", "--no-timing",
+               "--out", str(out)])
+    assert rc == 0
+    assert out.read_text() == golden_meta["fixtures"]["no_timing"]["raw"]

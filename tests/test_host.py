@@ -213,3 +213,17 @@ def test_product_path_does_not_import_the_oracle():
     pkg = ROOT / "paper_1609_09358_b200"
     for p in pkg.rglob("*.py"):
         assert not re.search(r"^\s*(from|import)\s+oracle", p.read_text(), re.M), p
+
+
+def test_cli_parser_matches_reference_flags():
+    from paper_1609_09358_b200.cli import _parse_ebno_range, build_parser, config_from_args
+
+    assert _parse_ebno_range("1:4:0.5") == (1.0, 1.5, 2.0, 2.5, 3.0, 3.5, 4.0)
+    assert _parse_ebno_range("2:3:1") == (2.0, 3.0)
+    args = build_parser().parse_args(["--n", "1024", "--rate", "0.5", "--decoder", "hybrid", "--list-size", "32",
+                                      "--ebno-list", "1,2.5", "--crc", "none", "--no-timing"])
+    cfg = config_from_args(args)
+    assert (cfg.N, cfg.k, cfg.decoder, cfg.list_size, cfg.crc_width) == (1024, 512, "hybrid", 32, 0)
+    assert cfg.ebno_points == (1.0, 2.5) and cfg.measure_time is False
+    with pytest.raises(SystemExit):
+        build_parser().parse_args(["--n", "8", "--k", "4", "--rate", "0.5", "--ebno", "1:2:1"])
