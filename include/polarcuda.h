@@ -53,7 +53,8 @@ typedef struct pc_code {
     int32_t crc_width;           /* 0 (no CRC), 8, 16 or 24 */
     uint32_t crc_offset;         /* CRC register after k zero bits (0 for init = 0) */
     uint32_t enc_crc_offset;     /* CRC register after m zero bits */
-    int32_t reserved;
+    int32_t first_info;          /* info_pos[0] (host copy): SCL decodes the all-frozen prefix
+                                    before it element-parallel; 0 disables that path */
     const uint32_t *frozen_bits; /* [ceil(N/32)]  1 = frozen                      */
     const uint32_t *crc_cols;    /* [N] register contribution of a 1 at position i */
     const int32_t *info_pos;     /* [k] ascending non-frozen positions             */

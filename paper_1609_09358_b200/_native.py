@@ -44,7 +44,7 @@ class PcCode(C.Structure):
         ("crc_width", C.c_int32),
         ("crc_offset", C.c_uint32),
         ("enc_crc_offset", C.c_uint32),
-        ("reserved", C.c_int32),
+        ("first_info", C.c_int32),
         ("frozen_bits", C.c_void_p),
         ("crc_cols", C.c_void_p),
         ("info_pos", C.c_void_p),
@@ -189,7 +189,7 @@ class DeviceCode:
             code.crc_width,
             off,
             eoff,
-            0,
+            int(code.info_positions[0]) if code.k > 0 else 0,
             ptr(self.frozen_bits),
             ptr(self.crc_cols),
             ptr(self.info_pos),

@@ -13,6 +13,8 @@ static int check_code(const pc_code_t *c)
         return PC_ERR_INVALID;
     if (c->frozen_bits == nullptr || c->info_pos == nullptr)
         return PC_ERR_INVALID;
+    if (c->first_info < 0 || c->first_info >= c->N)
+        return PC_ERR_INVALID;
     return PC_OK;
 }
 

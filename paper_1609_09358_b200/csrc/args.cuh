@@ -38,6 +38,7 @@ struct SclArgs {
     int32_t table_words; // CTA-shared frozen / decision-aided masks
     // v3 (scl3.cu) per-warp section offsets, in 32-bit words from the warp base
     int32_t o_ps, o_tb, o_tba, o_cand, o_wrow, o_ch;
+    int32_t prefix; // v3: frozen-prefix fast path enabled (L = 32 and 2N floats of scratch fit)
 };
 
 int launch_bp_decode(const BpArgs &a, int g_mode, int tpf, int kernel, cudaStream_t s);

@@ -40,6 +40,7 @@ __device__ __forceinline__ uint32_t bit_of(const uint32_t *words, int i) { retur
 struct Code {
     int32_t N, n, k, m, crc_width;
     uint32_t crc_offset, enc_crc_offset;
+    int32_t first_info;
     const uint32_t *frozen_bits, *crc_cols;
     const int32_t *info_pos;
     const uint32_t *enc_cols, *da_bits;
@@ -55,6 +56,7 @@ inline Code to_device_code(const pc_code_t &c)
     d.crc_width = c.crc_width;
     d.crc_offset = c.crc_offset;
     d.enc_crc_offset = c.enc_crc_offset;
+    d.first_info = c.first_info;
     d.frozen_bits = c.frozen_bits;
     d.crc_cols = c.crc_cols;
     d.info_pos = c.info_pos;

@@ -55,6 +55,10 @@ int scl3_prepare(SclArgs &a, int L, int nv_req)
         o += F * a.code.N;
     a.warp_words = (o + 3) & ~3;
     a.table_words = 0;
+    // The frozen prefix is decoded element-parallel in the slots of lanes 1..31
+    // (unused while one path is alive): two ping-pong buffers of N floats.
+    const char *envp = getenv("PC_SCL_PREFIX"); // dev knob
+    a.prefix = (L == 32 && 2 * a.code.N <= 31 * a.ss && (envp == nullptr || atoi(envp) != 0)) ? 1 : 0;
     return PC_OK;
 }
 

@@ -117,6 +117,57 @@ __device__ __forceinline__ int gsum_i(int v)
     }
 }
 
+// Frozen prefix (leaves [0, E), one path alive): every decision is 0, so every
+// node value depends on the channel only and the tree is walked breadth-first,
+// element-parallel over the warp, in the slots of lanes 1..31 (unused while one
+// path is alive).  Same f / g(u = 0) arithmetic as the block walk; the last node
+// of each stored level goes to lane 0's slot, lane 0's partial sums are zeroed
+// (the codeword of an all-frozen prefix is 0), and the returned metric is the
+// same sequential sum of the u = 0 increments: the state is bit-identical to
+// walking the E / 2^T blocks.
+template <bool FEX>
+__device__ __noinline__ float frozen_prefix(const float *ch, float *llr, uint32_t *ps, int n, int tp, int ss, int psw,
+                                            int E, int metric_exact, int lane)
+{
+    const int N = 1 << n;
+    float *sA = llr + ss, *sB = sA + N;
+    const float *Pv = ch;
+    float *out = sA;
+    for (int s = n - 1; s >= 0; --s) {
+        const int w = 1 << s;
+        const int tot = ((E + w - 1) >> s) << s;
+        for (int idx = lane; idx < tot; idx += 32) {
+            const int k = idx >> s, t = idx & (w - 1);
+            const float *pp = Pv + ((k >> 1) << (s + 1));
+            const float A = pp[t], Bv = pp[t + w];
+            out[idx] = (k & 1) ? Bv + A : scl_f<FEX>(A, Bv);
+        }
+        __syncwarp();
+        if (s >= T + 1 && s <= tp) {
+            const int kk = (E - 1) >> s;
+            for (int t = lane; t < w; t += 32)
+                llr[llo(s) + t] = out[(kk << s) + t];
+        }
+        Pv = out;
+        out = (out == sA) ? sB : sA;
+        __syncwarp();
+    }
+    for (int i = lane; i < E; i += 32) {
+        float i0v, i1v;
+        metric_incs(Pv[i], metric_exact, i0v, i1v);
+        out[i] = i0v;
+    }
+    for (int q = lane; q < psw; q += 32)
+        ps[q] = 0u;
+    __syncwarp();
+    float m = 0.0f;
+    if (lane == 0)
+        for (int i = 0; i < E; ++i)
+            m += out[i];
+    __syncwarp();
+    return m;
+}
+
 } // namespace s3
 
 template <int L, bool FEX, int NV>
@@ -148,6 +199,11 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
     const uint32_t *damg = a.code.da_bits;
     const uint32_t *colg = a.code.crc_cols;
     const bool use_crc = a.code.crc_width > 0;
+
+    // blocks before the first non-frozen position: decoded element-parallel (below)
+    // (from the code struct, not a device load: a load here costs the block walk
+    // ~20% through its code generation)
+    const int nb0 = (L == 32 && a.prefix) ? a.code.first_info >> T : 0;
 
     uint32_t lp32 = 0;
     uint64_t lp64 = 0;
@@ -185,8 +241,17 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
         float metric = 0.0f;
         uint32_t syn = 0u, cur = 0u, anc = (uint32_t)lane;
 
+        int b_begin = 0;
+        if (L == 32 && nb0 > 0 && grp_live) {
+            // ---- frozen prefix (leaves [0, E), one path): decoded element-parallel by
+            // the whole warp (s3::frozen_prefix; out of line so the block walk's code
+            // generation is not disturbed)
+            metric = frozen_prefix<FEX>(ch, llr, ps, n, tp, ss, psw, nb0 << T, a.metric_exact, lane);
+            b_begin = nb0;
+        }
+
         const int nblk = N >> T;
-        for (int b = 0; b < nblk; ++b) {
+        for (int b = b_begin; b < nblk; ++b) {
             const int i0 = b << T;
             const bool act0 = pl < P;
             // ================= upper descent: level T into registers =================
