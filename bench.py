@@ -40,7 +40,14 @@ METRIC = "decoded info Gbit/s, hybrid BP+SCL N=1024 L=32, vs Eb/N0; p50 frame la
 EBNO = (1.0, 1.5, 2.0, 2.5, 3.0, 3.5, 4.0)
 N, K, LIST, IMAX = 1024, 512, 32, 50
 SEED = 20240917
-MUFU_PER_G = 3.5  # bp_pe2: 3 EX2 + 4 LG2 per processing element (2 exact g)
+def mufu_per_alg_g(n: int, keep: bool) -> float:
+    """MUFU ops K1 spends per ALGORITHMIC exact g (the reference's 2nN per
+    frame-iteration, bp.py:138-161).  A PE (two g) costs 7 MUFU (3 EX2 + 4 LG2,
+    bp_math.cuh); with the kept exponentials (N <= 2048) the L-sweep PEs at
+    boundaries 1..n-1 cost 6; R[n] (never read) is not computed."""
+    r = (n - 1) * 7
+    l_ = 7 + (n - 1) * (6 if keep else 7)
+    return (r + l_) / 2 / (2 * n)  # per PE-pair of sweeps -> per g, over the 2n algorithmic g per node pair
 WORKLOAD = "hybrid BP->SCL N=1024 K=512 (496 payload + CRC-16) L=32 i_max=50, Eb/N0 1-4 dB step 0.5"
 
 
@@ -257,7 +264,8 @@ def run_gpu(args):
     except Exception:
         pass
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak = sms * 16 * peak_mhz * 1e6 / MUFU_PER_G / 1e9  # MUFU ops/s / MUFU per exact g, in Gg/s
+    mpg = mufu_per_alg_g(code.n, True)
+    peak = sms * 16 * peak_mhz * 1e6 / mpg / 1e9  # MUFU ops/s / MUFU per algorithmic exact g, in Gg/s
     traffic = None
     prof = ROOT / "profiles" / "bp_kernel_ncu.json"
     if prof.exists():
@@ -269,8 +277,10 @@ def run_gpu(args):
         "bound": "xu", "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
         "traffic": traffic, "kernel": "k_bp2<10,256,0> (register/shuffle BP, TPF=256)",
         "note": "exact-g node updates/s of K1 vs the MUFU (XU) pipe bound: 148 SM x 16 MUFU/clk x sm_max_mhz / "
-                "3.5 MUFU per g (3 EX2 + 4 LG2 per PE); HBM is <1% (4.2 KB/frame)",
-        "peak_at_measured_clock": (sms * 16 * ck["sm_mhz"] * 1e6 / MUFU_PER_G / 1e9) if ck.get("sm_mhz") else None,
+                "MUFU per algorithmic g (2nN per frame-iteration, the reference's count; 7 MUFU per PE, 6 in the "
+                "L sweep with kept exponentials, R[n] not computed); HBM is <1% (4.2 KB/frame)",
+        "peak_at_measured_clock": (sms * 16 * ck["sm_mhz"] * 1e6 / mpg / 1e9) if ck.get("sm_mhz") else None,
+        "mufu_per_algorithmic_g": mpg,
         # K1's own HBM traffic: read the LLRs, write payload + iters + flag + stamp per frame
         "hbm_gbs": len(EBNO) * B * (4 * N + 4 * MW + 4 + 1 + 8) / (bp_ms_step * 1e-3) / 1e9,
         "bp_share_of_step": bp_ms_step / (max_ms / args.steps),
@@ -346,14 +356,14 @@ def _gpu_common(args):
     return torch, dist, rank, world, local
 
 
-def _xu_peak_gg(torch, dev):
+def _xu_peak_gg(torch, dev, mpg):
     peak_mhz = 1965.0
     try:
         peak_mhz = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("sm_max_mhz", 1965.0))
     except Exception:
         pass
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    return sms * 16 * peak_mhz * 1e6 / MUFU_PER_G / 1e9
+    return sms * 16 * peak_mhz * 1e6 / mpg / 1e9
 
 
 def run_c4(args):
@@ -427,7 +437,7 @@ def run_c4(args):
     value = world * B * m * len(pts) * args.steps / (max_ms * 1e-3) / 1e9
     g_step = int(it_sum.sum()) * 2 * code.n * n4
     achieved = g_step / (sum(pt_ms) * 1e-3) / 1e9
-    peak = _xu_peak_gg(torch, dev)
+    peak = _xu_peak_gg(torch, dev, mufu_per_alg_g(code.n, False))  # no kept exponentials at N = 4096
     # e2e: pinned host LLRs -> device, decode, payload + flags -> host, every step
     host = [torch.empty((B, n4), dtype=torch.float32, pin_memory=True) for _ in pts]
     for p in range(len(pts)):
@@ -505,7 +515,8 @@ def run_c4(args):
                        "ber": float(errs_h[p, 0]) / (B * m)} for p, eb in enumerate(pts)],
             "roofline": {"bound": "xu", "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
                          "traffic": None, "kernel": "k_bp2<12,1024,0> (register/shuffle BP, 1024 threads/frame)",
-                         "note": "exact-g node updates/s (2nN per frame-iteration) vs 148 SM x 16 MUFU/clk / 3.5 MUFU per g"},
+                         "note": "exact-g node updates/s (2nN per frame-iteration) vs 148 SM x 16 MUFU/clk / "
+                                 "MUFU per algorithmic g (7 per PE, R[n] not computed)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "Gbit/s", "h2d_bytes_per_step": B * n4 * 4 * len(pts),
                     "d2h_bytes_per_step": B * (MW * 4 + 1) * len(pts)},

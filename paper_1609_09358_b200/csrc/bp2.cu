@@ -31,6 +31,21 @@ struct ilog2<1> {
     static constexpr int value = 0;
 };
 
+// Exponential reuse (GMODE 0): the R sweep's 2^-|a| of every PE at boundaries
+// 2..n-1 is kept in shared memory (one float per PE) and reused by the L sweep,
+// where a is the PE's second operand: 6 MUFU instead of 7 for those PEs.
+__host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+__host__ __device__ constexpr int bp2_base_bytes(int logn, int tpf)
+{
+    // R rows bw..n-1 and L rows bw..n (bw = log2 Q + 5, i.e. n - bw = log2 TPF - 5), plus N bytes of decisions
+    return (2 * (ilog2c(tpf) - 5) + 1) * (1 << logn) * 4 + (1 << logn);
+}
+__host__ __device__ constexpr int bp2_pas_bytes(int logn, int tpf) { return (logn - 2) * ((1 << logn) / tpf / 2) * tpf * 4; }
+__host__ __device__ constexpr bool bp2_pas(int logn, int tpf, int gmode)
+{
+    return gmode == 0 && bp2_base_bytes(logn, tpf) + bp2_pas_bytes(logn, tpf) <= 200 * 1024;
+}
+
 template <int LOGN, int TPF, int GMODE>
 __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
 {
@@ -50,6 +65,8 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
     float *Rs = sm;           // R[BW + r], r < NSR
     float *Ls = sm + NSR * N; // L[BW + r], r < NSL
     uint8_t *ub = reinterpret_cast<uint8_t *>(Ls + NSL * N);
+    constexpr bool PAS = bp2_pas(LOGN, TPF, GMODE);
+    float *Pa = Ls + NSL * N + N / 4; // kept exponentials, [(j - 2) * Q/2 + k][tid]
     __shared__ uint32_t frz[NW];
     __shared__ uint32_t red[NWARP];
 
@@ -91,6 +108,8 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
 
     // compile-time stage accessors (every loop below is fully unrolled, so the
     // register arrays are indexed with constants)
+#define PA(j, k) Pa[(((j) - 2) * (Q / 2) + (k)) * TPF + tid]
+    const float pprior = GMODE == 0 ? ex2_approx(-lim) : 0.0f; // 2^-|R[0]| of a frozen node
 #define RGET(s, r) ((s) == 0 ? pri[r] : ((s) <= NREG ? Rr[(s) > 0 ? (s) - 1 : 0][r] : Rs[((s) - BW) * N + base + (r)]))
 #define LGET(s, r) ((s) <= NREG ? Lr[(s) > 0 ? (s) - 1 : 0][r] : Ls[((s) - BW) * N + base + (r)])
 
@@ -109,7 +128,13 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                     continue;
                 const int r2 = r1 + h;
                 const float av = RGET(j - 1, r1), r2v = RGET(j - 1, r2), l1 = LGET(j, r1), l2 = LGET(j, r2);
-                bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, Rr[j - 1][r1], Rr[j - 1][r2]);
+                if (PAS && j >= 2) {
+                    float px;
+                    bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, Rr[j - 1][r1], Rr[j - 1][r2], px);
+                    PA(j, ((r1 >> j) << (j - 1)) | (r1 & (h - 1))) = px;
+                } else {
+                    bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, Rr[j - 1][r1], Rr[j - 1][r2]);
+                }
             }
         }
 #pragma unroll
@@ -133,7 +158,13 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 // (a, r2, l1, l2) of the PE at my node
                 const float av = hi ? pr : myR, r2v = hi ? myR : pr, l1 = hi ? pl : myL, l2 = hi ? myL : pl;
                 float o1, o2;
-                bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                if (PAS) {
+                    float px;
+                    bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, o1, o2, px);
+                    PA(j, k) = px;
+                } else {
+                    bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                }
                 const float back = __shfl_xor_sync(0xffffffffu, hi ? o1 : o2, msk); // my output the partner computed
                 Rn[k] = hi ? back : o1;
                 Rn[k + Q / 2] = hi ? o2 : back;
@@ -159,7 +190,13 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
                 const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
                 float o1, o2;
-                bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                if (PAS) {
+                    float px;
+                    bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, o1, o2, px);
+                    PA(j, q) = px;
+                } else {
+                    bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                }
                 Rd[i1] = o1;
                 Rd[i2] = o2;
             }
@@ -178,7 +215,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
                 const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
                 float o1, o2;
-                bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                if (PAS && j <= LOGN - 1)
+                    bp_pe2_p2(l1, l2 + r2v, av, PA(j, q), l2, lim, o1, o2);
+                else
+                    bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
                 Ld[i1] = o1;
                 Ld[i2] = o2;
             }
@@ -200,7 +240,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 // (a, r2, l1, l2) of the PE at my node
                 const float av = hi ? pr : myR, r2v = hi ? myR : pr, l1 = hi ? pl : myL, l2 = hi ? myL : pl;
                 float o1, o2;
-                bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                if (PAS && j <= LOGN - 1)
+                    bp_pe2_p2(l1, l2 + r2v, av, PA(j, k), l2, lim, o1, o2);
+                else
+                    bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
                 const float back = __shfl_xor_sync(0xffffffffu, hi ? o1 : o2, msk); // my output the partner computed
                 Ln[k] = hi ? back : o1;
                 Ln[k + Q / 2] = hi ? o2 : back;
@@ -219,7 +262,12 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 const int r2 = r1 + h;
                 const float av = RGET(j - 1, r1), r2v = RGET(j - 1, r2), l1 = LGET(j, r1), l2 = LGET(j, r2);
                 float o1, o2;
-                bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                if (PAS && j >= 2)
+                    bp_pe2_p2(l1, l2 + r2v, av, PA(j, ((r1 >> j) << (j - 1)) | (r1 & (h - 1))), l2, lim, o1, o2);
+                else if (PAS)
+                    bp_pe2_p2(l1, l2 + r2v, av, av != 0.0f ? pprior : 1.0f, l2, lim, o1, o2); // R[0] prior
+                else
+                    bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
                 if (j > 1) {
                     Lr[j - 2][r1] = o1;
                     Lr[j - 2][r2] = o2;
@@ -286,6 +334,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
 
 #undef RGET
 #undef LGET
+#undef PA
 
 static size_t bp2_smem_bytes(int logn, int tpf)
 {
@@ -301,7 +350,7 @@ template <int LOGN, int TPF, int GMODE>
 static int launch_bp2_t(const BpArgs &a, cudaStream_t s)
 {
     auto kern = k_bp2<LOGN, TPF, GMODE>;
-    const size_t smem = bp2_smem_bytes(LOGN, TPF);
+    const size_t smem = bp2_smem_bytes(LOGN, TPF) + (bp2_pas(LOGN, TPF, GMODE) ? bp2_pas_bytes(LOGN, TPF) : 0);
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return PC_ERR_CUDA;

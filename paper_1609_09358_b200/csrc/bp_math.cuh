@@ -46,6 +46,25 @@ __host__ __device__ constexpr float bp_unit_in() { return GMODE == 0 ? PC_LOG2E 
 template <int GMODE>
 __host__ __device__ constexpr float bp_unit_out() { return GMODE == 0 ? PC_LN2 : 1.0f; }
 
+// Core of a PE update with the three exponentials p = 2^-|v| given (GMODE 0).
+__device__ __forceinline__ void bp_pe2_core(float x, float y1, float y2, float px, float p1, float p2, float add,
+                                            float lim, float &o1, float &o2)
+{
+    const float ax = fabsf(x), a1 = fabsf(y1), a2 = fabsf(y2);
+    const float X1 = fmaf(px, p1, 1.0f), X2 = fmaf(px, p2, 1.0f);
+    float m1 = lg2_approx(X1) - lg2_approx(px + p1); // log2 units: |g'| = lg2(1 + px py) - lg2(px + py)
+    float m2 = lg2_approx(X2) - lg2_approx(px + p2);
+    // (no upper clamp at min(|x|, |y|): the computed value exceeds it by rounding
+    // noise only, and every message is clipped or feeds a clipped one)
+    const float lb1 = fminf(fminf(ax, a1), 0.0009765625f) * fmaf(-0.5f, X1, 1.0f);
+    const float lb2 = fminf(fminf(ax, a2), 0.0009765625f) * fmaf(-0.5f, X2, 1.0f);
+    m1 = fmaxf(m1, lb1);
+    m2 = fmaxf(m2, lb2);
+    o1 = __uint_as_float(__float_as_uint(m1) ^ ((__float_as_uint(x) ^ __float_as_uint(y1)) & 0x80000000u));
+    const float g2 = __uint_as_float(__float_as_uint(m2) ^ ((__float_as_uint(x) ^ __float_as_uint(y2)) & 0x80000000u));
+    o2 = clampf(g2 + add, lim);
+}
+
 template <int GMODE>
 __device__ __forceinline__ void bp_pe2(float x, float y1, float y2, float add, float lim, float &o1, float &o2)
 {
@@ -54,28 +73,33 @@ __device__ __forceinline__ void bp_pe2(float x, float y1, float y2, float add, f
         o2 = clampf(bp_g<0>(x, y2, lim) + add, lim);
         return;
     }
-    const float ax = fabsf(x), a1 = fabsf(y1), a2 = fabsf(y2);
-    float m1, m2;
-    if (GMODE == 0) { // log2 units: p = 2^-|v'|, |g'| = lg2(1 + px py) - lg2(px + py)
-        const float px = ex2_approx(-ax);
-        const float p1 = ex2_approx(-a1);
-        const float p2 = ex2_approx(-a2);
-        const float X1 = fmaf(px, p1, 1.0f), X2 = fmaf(px, p2, 1.0f);
-        m1 = lg2_approx(X1) - lg2_approx(px + p1);
-        m2 = lg2_approx(X2) - lg2_approx(px + p2);
-        // (no upper clamp at min(|x|, |y|): the computed value exceeds it by rounding
-        // noise only, and every message is clipped or feeds a clipped one)
-        const float lb1 = fminf(fminf(ax, a1), 0.0009765625f) * fmaf(-0.5f, X1, 1.0f);
-        const float lb2 = fminf(fminf(ax, a2), 0.0009765625f) * fmaf(-0.5f, X2, 1.0f);
-        m1 = fmaxf(m1, lb1);
-        m2 = fmaxf(m2, lb2);
-    } else {
-        m1 = (x == 0.0f || y1 == 0.0f) ? 0.0f : fminf(ax, a1);
-        m2 = (x == 0.0f || y2 == 0.0f) ? 0.0f : fminf(ax, a2);
+    if (GMODE == 0) { // log2 units: p = 2^-|v'|
+        bp_pe2_core(x, y1, y2, ex2_approx(-fabsf(x)), ex2_approx(-fabsf(y1)), ex2_approx(-fabsf(y2)), add, lim, o1,
+                    o2);
+        return;
     }
+    const float ax = fabsf(x), a1 = fabsf(y1), a2 = fabsf(y2);
+    const float m1 = (x == 0.0f || y1 == 0.0f) ? 0.0f : fminf(ax, a1);
+    const float m2 = (x == 0.0f || y2 == 0.0f) ? 0.0f : fminf(ax, a2);
     o1 = __uint_as_float(__float_as_uint(m1) ^ ((__float_as_uint(x) ^ __float_as_uint(y1)) & 0x80000000u));
     const float g2 = __uint_as_float(__float_as_uint(m2) ^ ((__float_as_uint(x) ^ __float_as_uint(y2)) & 0x80000000u));
     o2 = clampf(g2 + add, lim);
+}
+
+// GMODE 0 R-sweep PE that also returns px = 2^-|a| (x = a) for reuse by the
+// L sweep at the same boundary, where a is the second operand (bp_pe2_p2).
+__device__ __forceinline__ void bp_pe2_keep(float x, float y1, float y2, float add, float lim, float &o1, float &o2,
+                                            float &px)
+{
+    px = ex2_approx(-fabsf(x));
+    bp_pe2_core(x, y1, y2, px, ex2_approx(-fabsf(y1)), ex2_approx(-fabsf(y2)), add, lim, o1, o2);
+}
+
+// GMODE 0 L-sweep PE with p2 = 2^-|y2| supplied (y2 = a, kept from the R sweep).
+__device__ __forceinline__ void bp_pe2_p2(float x, float y1, float y2, float p2, float add, float lim, float &o1,
+                                          float &o2)
+{
+    bp_pe2_core(x, y1, y2, ex2_approx(-fabsf(x)), ex2_approx(-fabsf(y1)), p2, add, lim, o1, o2);
 }
 
 } // namespace pc
