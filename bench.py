@@ -293,11 +293,12 @@ def run_gpu(args):
         for p in range(len(EBNO)):
             host[p].copy_(llr[p])
         torch.cuda.synchronize()
-        dec.decode_host_many(host)  # warm-up (allocates the double buffers)
+        dec.decode_host_many(host * args.steps)  # warm-up: allocates the double and pinned result buffers
         barrier()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            dec.decode_host_many(host)  # H2D of point p+1 overlaps the decode of point p
+        # one stream of host batches (all steps x points): the H2D of batch i+1
+        # overlaps the decode of batch i, so only the first copy is exposed
+        dec.decode_host_many(host * args.steps)
         barrier()
         e2e_s = time.perf_counter() - t0
         e2e_val = world * bits_step * args.steps / max_over_ranks(e2e_s, device=dev) / 1e9
@@ -447,26 +448,28 @@ def run_c4(args):
     dbufs = [torch.empty((B, n4), dtype=torch.float32, device=dev) for _ in range(2)]
     s_copy = torch.cuda.Stream(device=dev)
 
-    def e2e_step():
-        # H2D of point p+1 on a copy stream overlaps the decode of point p
+    def e2e_run(nsteps):
+        # one stream of host batches (nsteps x points): the H2D of batch i+1 on a
+        # copy stream overlaps the decode of batch i
         cur = torch.cuda.current_stream(dev)
+        seq = [p for _ in range(nsteps) for p in range(len(pts))]
         h2d, done = [], []
 
         def issue(i):
             with torch.cuda.stream(s_copy):
                 if i >= 2:
                     s_copy.wait_event(done[i - 2])
-                dbufs[i % 2].copy_(host[i], non_blocking=True)
+                dbufs[i % 2].copy_(host[seq[i]], non_blocking=True)
                 e = torch.cuda.Event()
                 e.record(s_copy)
                 h2d.append(e)
 
         issue(0)
-        for p in range(len(pts)):
-            if p + 1 < len(pts):
-                issue(p + 1)
-            cur.wait_event(h2d[p])
-            nat.check(lib.pc_bp_decode(dbufs[p % 2].data_ptr(), B, dc.ref, ctypes.byref(cfg), None, pay.data_ptr(),
+        for i, p in enumerate(seq):
+            if i + 1 < len(seq):
+                issue(i + 1)
+            cur.wait_event(h2d[i])
+            nat.check(lib.pc_bp_decode(dbufs[i % 2].data_ptr(), B, dc.ref, ctypes.byref(cfg), None, pay.data_ptr(),
                                        None, None, iters[p].data_ptr(), conv[p].data_ptr(), None, st), "pc_bp_decode")
             e = torch.cuda.Event()
             e.record(cur)
@@ -475,11 +478,10 @@ def run_c4(args):
             conv_h[p].copy_(conv[p], non_blocking=True)
         torch.cuda.synchronize()
 
-    e2e_step()
+    e2e_run(1)
     barrier()
     te = time.perf_counter()
-    for _ in range(args.steps):
-        e2e_step()
+    e2e_run(args.steps)
     barrier()
     e2e_val = world * B * m * len(pts) * args.steps / max_over_ranks(time.perf_counter() - te, device=dev) / 1e9
     if rank == 0:

@@ -210,7 +210,8 @@ class HybridDecoder:
         (two device input buffers), each batch's payload words and converged
         flags are read back right after its decode.  Returns a list of
         (payload words uint32 [B_i, ceil(m/32)], converged bool [B_i]) numpy
-        arrays, in order.  Results equal ``decode_host`` per batch."""
+        arrays, in order: views of pinned buffers that the next call reuses (copy
+        them to keep them).  Results equal ``decode_host`` per batch."""
         torch = self.torch
         dev = self.device
         if not batches:
@@ -247,13 +248,24 @@ class HybridDecoder:
             ev = torch.cuda.Event()
             ev.record(cur)
             done[i] = ev
-            pay = torch.empty((B, self.MW), dtype=torch.int32, pin_memory=True)
-            conv = torch.empty(B, dtype=torch.uint8, pin_memory=True)
+            pay, conv = self._pinned_out(i, B)
             pay.copy_(self.payload[:B], non_blocking=True)
             conv.copy_(self.conv[:B], non_blocking=True)
             outs.append((pay, conv))
         cur.synchronize()
-        return [(p.numpy().view(np.uint32), c.numpy().astype(bool)) for p, c in outs]
+        return [(p.numpy().view(np.uint32), c.numpy().view(np.bool_)) for p, c in outs]
+
+    def _pinned_out(self, i: int, B: int):
+        """Pinned host result buffers for batch slot i (allocated once; pinning is slow)."""
+        torch = self.torch
+        pool = getattr(self, "_pin_pool", None)
+        if pool is None:
+            pool = self._pin_pool = []
+        while len(pool) <= i:
+            pool.append((torch.empty((self.capacity, self.MW), dtype=torch.int32, pin_memory=True),
+                         torch.empty(self.capacity, dtype=torch.uint8, pin_memory=True)))
+        pay, conv = pool[i]
+        return pay[:B], conv[:B]
 
     def _st(self, s) -> int:
         return int(s.cuda_stream)
