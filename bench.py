@@ -577,7 +577,7 @@ def run_c5(args):
                     nat.check(lib.pc_stamp(t0s.data_ptr(), st), "stamp")
                 nat.check(lib.pc_scl_decode(llr.data_ptr(), nf, None, None, dc.ref, ctypes.byref(cfg), None,
                                             pay.data_ptr(), None, None, None, tdone.data_ptr() if stamp else None,
-                                            dc.workspace.data_ptr(), st), "pc_scl_decode")
+                                            dc.scl_workspace(cfg).data_ptr(), st), "pc_scl_decode")
 
             for _ in range(args.warmup):
                 dec(B)

@@ -117,7 +117,12 @@ int pc_bp_iterate(float *l_msgs, float *r_msgs, int32_t B, const pc_code_t *code
  * written per frame index do not depend on it. */
 int pc_compact(const uint8_t *converged, int32_t B, int32_t *queue, int32_t *count, void *workspace, void *stream);
 
+/* Bytes of device workspace pc_scl_decode needs for this code and
+ * configuration (counters + the K3 decision traceback); -1 on bad arguments. */
+int64_t pc_scl_workspace_bytes(const pc_code_t *code, const pc_scl_cfg_t *cfg);
+
 /* Batched SCL decode with the CRC-aided winner (scl.py:151-197).
+ * workspace: at least pc_scl_workspace_bytes(code, cfg) bytes of device memory.
  * Frames decoded: queue[0..*count-1] (queue, count device) or 0..B-1 when
  * queue is NULL.  Outputs are indexed by FRAME, so the hybrid writes them
  * into the same per-frame arrays as pc_bp_decode.

@@ -28,6 +28,7 @@ EXPORTS = (
     "pc_bp_iterate",
     "pc_compact",
     "pc_scl_decode",
+    "pc_scl_workspace_bytes",
     "pc_encode",
     "pc_gen_frames",
     "pc_count_errors",
@@ -103,6 +104,7 @@ def load():
         "pc_bp_iterate": (i32, [vp, vp, i32, vp, vp, vp]),
         "pc_compact": (i32, [vp, i32, vp, vp, vp, vp]),
         "pc_scl_decode": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "pc_scl_workspace_bytes": (i64, [vp, vp]),
         "pc_encode": (i32, [vp, i32, vp, vp, vp]),
         "pc_gen_frames": (i32, [u64, i32, i64, i32, f32, vp, vp, vp, vp]),
         "pc_count_errors": (i32, [vp, vp, i32, i32, vp, vp]),
@@ -201,6 +203,19 @@ class DeviceCode:
     @property
     def ref(self):
         return C.byref(self.struct)
+
+    def scl_workspace(self, ncfg):
+        """Device workspace for pc_scl_decode with this code and PcSclCfg (cached by size)."""
+        import torch
+
+        nbytes = int(load().pc_scl_workspace_bytes(self.ref, C.byref(ncfg)))
+        if nbytes < 0:
+            raise RuntimeError("pc_scl_workspace_bytes rejected the configuration")
+        ws = getattr(self, "_scl_ws", None)
+        if ws is None or ws.numel() * 4 < nbytes:
+            ws = torch.zeros((nbytes + 3) // 4, dtype=torch.int32, device=self.device)
+            self._scl_ws = ws
+        return ws
 
     def with_da(self, da_mask):
         """Same code with a decision-aided position mask (SclConfig.da_threshold)."""

@@ -132,6 +132,7 @@ int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32
     a.sel = sel_by_crc;
     a.t_done = t_done;
     a.work = reinterpret_cast<int32_t *>(workspace);
+    a.tbg = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(workspace) + 256);
     if (cfg->kernel < 0 || cfg->kernel > 2)
         return PC_ERR_INVALID;
     int nv = cfg->virtual_levels;
@@ -149,6 +150,24 @@ int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32
         nv = code->n >= 12 ? 4 : (code->n >= 10 ? 3 : (code->n >= 8 ? 2 : 0));
     scl_prepare(a, nv);
     return launch_scl(a, L, cfg->warps_per_cta, (cudaStream_t)stream);
+}
+
+int64_t pc_scl_workspace_bytes(const pc_code_t *code, const pc_scl_cfg_t *cfg)
+{
+    if (check_code(code) || cfg == nullptr || cfg->L < 1 || cfg->L > PC_MAX_LIST || (cfg->L & (cfg->L - 1)))
+        return -1;
+    SclArgs a{};
+    a.code = to_device_code(*code);
+    a.B = 1;
+    if (cfg->kernel != 1 && scl3_eligible(a, cfg->L)) {
+        int nv = cfg->virtual_levels;
+        if (nv < 0)
+            nv = code->n >= 10 ? 3 : (code->n >= 8 ? 2 : 0);
+        if (scl3_prepare(a, cfg->L, nv))
+            return -1;
+        return scl3_workspace_bytes(a, cfg->L, cfg->warps_per_cta);
+    }
+    return pc_workspace_bytes();
 }
 
 int pc_encode(const uint32_t *msg_bits, int32_t B, const pc_code_t *code, uint32_t *x_bits, void *stream)

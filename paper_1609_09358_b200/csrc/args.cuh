@@ -39,6 +39,7 @@ struct SclArgs {
     // v3 (scl3.cu) per-warp section offsets, in 32-bit words from the warp base
     int32_t o_ps, o_tb, o_tba, o_cand, o_wrow, o_ch;
     int32_t prefix; // v3: frozen-prefix fast path enabled (L = 32 and 2N floats of scratch fit)
+    uint32_t *tbg;  // v3: decision traceback in the caller's workspace (after the 256-byte counter block)
 };
 
 int launch_bp_decode(const BpArgs &a, int g_mode, int tpf, int kernel, cudaStream_t s);
@@ -50,6 +51,7 @@ int launch_scl(const SclArgs &a, int L, int wpc, cudaStream_t s);
 bool scl3_eligible(const SclArgs &a, int L);
 int scl3_prepare(SclArgs &a, int L, int nv_req);
 int launch_scl3(const SclArgs &a, int L, int wpc, cudaStream_t s);
+int64_t scl3_workspace_bytes(const SclArgs &a, int L, int wpc);
 int launch_compact(const uint8_t *conv, int B, int32_t *queue, int32_t *count, cudaStream_t s);
 int launch_gen(const Code &c, uint64_t seed, int point, int64_t frame0, int B, float sigma, uint32_t *msg, float *llr,
                cudaStream_t s);

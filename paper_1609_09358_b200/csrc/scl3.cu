@@ -40,10 +40,7 @@ int scl3_prepare(SclArgs &a, int L, int nv_req)
     int o = 32 * a.ss;
     a.o_ps = o;
     o += 32 * a.psw;
-    a.o_tb = o;
-    o += 32 * W;
-    a.o_tba = o;
-    o += 8 * W;
+    a.o_tb = a.o_tba = -1; // the traceback lives in the workspace (scl3_workspace_bytes)
     a.o_cand = o;
     o += 128; // per group 4L words: candidate metrics + indices
     a.o_wrow = o;
@@ -60,6 +57,29 @@ int scl3_prepare(SclArgs &a, int L, int nv_req)
     const char *envp = getenv("PC_SCL_PREFIX"); // dev knob
     a.prefix = (L == 32 && 2 * a.code.N <= 31 * a.ss && (envp == nullptr || atoi(envp) != 0)) ? 1 : 0;
     return PC_OK;
+}
+
+// Upper bound of the resident warps of a K3 v3 launch (shared memory is its
+// occupancy limit) times the per-warp traceback, plus the counter block.
+int64_t scl3_workspace_bytes(const SclArgs &a, int L, int wpc)
+{
+    (void)L;
+    if (wpc < 1 || wpc > 4)
+        wpc = 1;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    const int64_t per_cta = (int64_t)wpc * a.warp_words * 4 + 1024; // + the per-CTA reservation
+    int64_t ctas = (228 * 1024) / per_cta;
+    if (ctas > 32)
+        ctas = 32;
+    int64_t warps = ctas * wpc;
+    if (warps > 64)
+        warps = 64;
+    if (warps < wpc)
+        warps = wpc;
+    return 256 + (int64_t)sms * warps * a.uhs * 40 * 4;
 }
 
 int launch_scl3(const SclArgs &a, int L, int wpc, cudaStream_t s)

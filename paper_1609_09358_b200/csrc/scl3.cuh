@@ -182,8 +182,9 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
     uint32_t *wb = smw + (size_t)(threadIdx.x >> 5) * a.warp_words;
     float *llr = reinterpret_cast<float *>(wb);
     uint32_t *ps = wb + a.o_ps;
-    uint32_t *tb = wb + a.o_tb;
-    uint8_t *tba = reinterpret_cast<uint8_t *>(wb + a.o_tba);
+    // decision traceback of this warp in the workspace: W x 32 words + W x 32 ancestor bytes
+    uint32_t *tb = a.tbg + (size_t)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (size_t)W * 40;
+    uint8_t *tba = reinterpret_cast<uint8_t *>(tb + W * 32);
     float *cand = reinterpret_cast<float *>(wb + a.o_cand);
     uint32_t *wrow = wb + a.o_wrow;
     float *chs = reinterpret_cast<float *>(wb + a.o_ch);

@@ -175,7 +175,8 @@ class HybridDecoder:
         self.counts = torch.zeros(self.nchunks_max, dtype=torch.int32, **z)
         # stamps per chunk: [start, bp_end, scl_start, scl_end]
         self.stamps = torch.zeros((self.nchunks_max, 4), dtype=torch.int64, **z)
-        self.workspaces = torch.zeros((self.nchunks_max, 64), dtype=torch.int32, **z)
+        # one K3 workspace for all chunks: their SCL launches are ordered on one stream
+        self.scl_ws = self.dc_scl.scl_workspace(self.nscl)
         self.s_bp = torch.cuda.Stream(device=dev)
         # The list decoder's persistent warps get the higher stream priority, so
         # they take SM slots as soon as K1 CTAs (one frame each) retire and the
@@ -319,7 +320,7 @@ class HybridDecoder:
                 lib.pc_scl_decode(
                     base_llr + 4 * N * b0, nb, q, cnt, self.dc_scl.ref, scl_ref, None,
                     self.payload.data_ptr() + 4 * self.MW * b0, None, None, None,
-                    self.t_scl.data_ptr() + 8 * b0, self.workspaces[c].data_ptr(), ss,
+                    self.t_scl.data_ptr() + 8 * b0, self.scl_ws.data_ptr(), ss,
                 ),
                 "pc_scl_decode",
             )

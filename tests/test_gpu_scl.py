@@ -70,7 +70,7 @@ def test_virtual_levels_do_not_change_results(nv):
         u = torch.zeros_like(base.u_hat)
         mt = torch.zeros_like(base.metric)
         nat.check(nat.load().pc_scl_decode(x.data_ptr(), 48, None, None, dc.ref, ctypes.byref(cfg), u.data_ptr(),
-                                           None, mt.data_ptr(), None, None, None, dc.workspace.data_ptr(),
+                                           None, mt.data_ptr(), None, None, None, dc.scl_workspace(cfg).data_ptr(),
                                            nat.stream_handle()), "scl")
         assert torch.equal(u, base.u_hat)
         assert torch.equal(mt, base.metric)

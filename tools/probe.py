@@ -65,7 +65,7 @@ if "scl" in sections:
                 a, b = ev(), ev()
                 a.record()
                 nat.check(lib.pc_scl_decode(llr.data_ptr(), Bs, None, None, dc.ref, ctypes.byref(cfg), None,
-                                            pay.data_ptr(), None, None, None, None, dc.workspace.data_ptr(), st), "scl")
+                                            pay.data_ptr(), None, None, None, None, dc.scl_workspace(cfg).data_ptr(), st), "scl")
                 b.record()
                 torch.cuda.synchronize()
             ms = a.elapsed_time(b)

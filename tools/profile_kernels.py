@@ -34,6 +34,6 @@ nat.check(lib.pc_bp_decode(llr.data_ptr(), B_BP, dc.ref, ctypes.byref(cfg), None
                            it.data_ptr(), cv.data_ptr(), None, st), "bp")
 scfg = SclConfig(32).native()
 nat.check(lib.pc_scl_decode(llr.data_ptr(), B_SCL, None, None, dc.ref, ctypes.byref(scfg), None, pay.data_ptr(),
-                            None, None, None, None, dc.workspace.data_ptr(), st), "scl")
+                            None, None, None, None, dc.scl_workspace(scfg).data_ptr(), st), "scl")
 torch.cuda.synchronize()
 print("bp frames", B_BP, "iterations", int(it[:B_BP].sum().item()), "scl frames", B_SCL)

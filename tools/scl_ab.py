@@ -40,7 +40,7 @@ for kern in (1, 2):
         def run():
             nat.check(lib.pc_scl_decode(llr.data_ptr(), B, None, None, dc.ref, ctypes.byref(cfg), u.data_ptr(),
                                         pay.data_ptr(), mt.data_ptr(), ok.data_ptr(), None, None,
-                                        dc.workspace.data_ptr(), st), f"scl kernel={kern}")
+                                        dc.scl_workspace(cfg).data_ptr(), st), f"scl kernel={kern}")
 
         run()
         torch.cuda.synchronize()
