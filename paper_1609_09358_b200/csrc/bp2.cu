@@ -43,7 +43,7 @@ __host__ __device__ constexpr int bp2_base_bytes(int logn, int tpf)
 __host__ __device__ constexpr int bp2_pas_bytes(int logn, int tpf) { return (logn - 2) * ((1 << logn) / tpf / 2) * tpf * 4; }
 __host__ __device__ constexpr bool bp2_pas(int logn, int tpf, int gmode)
 {
-    return gmode == 0 && bp2_base_bytes(logn, tpf) + bp2_pas_bytes(logn, tpf) <= 200 * 1024;
+    return gmode == 0 && bp2_base_bytes(logn, tpf) + bp2_pas_bytes(logn, tpf) <= 225 * 1024;
 }
 
 template <int LOGN, int TPF, int GMODE>
@@ -365,7 +365,7 @@ static int launch_bp2_n(const BpArgs &a, int tpf, cudaStream_t s)
     constexpr int LO = N / 8 > 32 ? N / 8 : 32; // Q <= 8 nodes per thread (Q = 16 needs ~120+ registers)
     constexpr int HI = N / 2;                   // Q >= 2
     if (tpf <= 0)
-        tpf = N >= 4096 ? 1024 : (N / 4 >= 256 ? 256 : N / 4);
+        tpf = N >= 4096 ? 512 : (N / 4 >= 256 ? 256 : N / 4); // measured (tools/bp_tpf_probe.py)
     if (tpf < LO || tpf > HI)
         return PC_ERR_UNSUPPORTED;
 #define PC_BP2_CASE(T)                                                                                                 \
@@ -383,7 +383,8 @@ static int launch_bp2_n(const BpArgs &a, int tpf, cudaStream_t s)
 }
 
 // K1 v2 covers N = 128 .. 4096 with the crc / none stop rules and no soft_x.
-// N = 4096 runs one 1024-thread CTA per frame (Q = 4): 11 shared rows, 176 KB.
+// N = 4096 runs one 512-thread CTA per frame (Q = 8): 9 shared rows (144 KB) plus
+// 80 KB of kept exponentials, one CTA per SM.
 bool bp2_eligible(const BpArgs &a, int tpf)
 {
     const int N = a.code.N;
