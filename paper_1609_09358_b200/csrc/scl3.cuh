@@ -437,23 +437,36 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                                     um[qb] = bv;
                                     ui[qb] = bi;
                                 }
-                                if (nu & 1)
-                                    um[nu] = INFINITY; // pad to pairs
-                                __syncwarp();
                                 int rg = 0, rb = 0;
-                                const int numax = __reduce_max_sync(FULL, nu);
-                                for (int q = 0; q < numax; q += 2) {
-                                    const float2 v = *reinterpret_cast<const float2 *>(um + q);
-                                    const bool l0 = q < nu, l1v = q + 1 < nu;
-                                    rg += (l0 && v.x < gv) + (l1v && v.y < gv);
-                                    rb += (l0 && v.x < bv) + (l1v && v.y < bv);
+                                if constexpr (L == 32) {
+                                    // one group: nu is warp-uniform; pad U to a multiple of 4 with +inf
+                                    if (lane < ((-nu) & 3))
+                                        um[nu + lane] = INFINITY;
+                                    __syncwarp();
+                                    for (int q = 0; q < nu; q += 4) {
+                                        const float4 v = *reinterpret_cast<const float4 *>(um + q);
+                                        rg += (v.x < gv) + (v.y < gv) + (v.z < gv) + (v.w < gv);
+                                        rb += (v.x < bv) + (v.y < bv) + (v.z < bv) + (v.w < bv);
+                                    }
+                                } else {
+                                    if (nu & 1)
+                                        um[nu] = INFINITY; // pad to pairs
+                                    __syncwarp();
+                                    const int numax = __reduce_max_sync(FULL, nu);
+                                    for (int q = 0; q < numax; q += 2) {
+                                        const float2 v = *reinterpret_cast<const float2 *>(um + q);
+                                        const bool l0 = q < nu, l1v = q + 1 < nu;
+                                        rg += (l0 && v.x < gv) + (l1v && v.y < gv);
+                                        rb += (l0 && v.x < bv) + (l1v && v.y < bv);
+                                    }
                                 }
                                 // no ties inside U <=> the strict ranks of its nu elements sum to nu(nu-1)/2
                                 const int rsum = gsum_i<L>((hiG ? rg : 0) + (loB ? rb : 0));
                                 if (__any_sync(FULL, rsum != nu * (nu - 1) / 2)) {
                                     rg = 0;
                                     rb = 0;
-                                    for (int q = 0; q < numax; ++q) {
+                                    const int numax2 = __reduce_max_sync(FULL, nu);
+                                    for (int q = 0; q < numax2; ++q) {
                                         const float v = um[q];
                                         const int vi = ui[q];
                                         const bool live = q < nu;
@@ -483,12 +496,8 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                         metric = k0 ? c0 : c1;
                     } else {
                         const int r = act ? __popc(freeM & ((1u << pl) - 1u)) : nf + (pl - P);
-                        if (r < nd) {
-                            uint32_t m = dupM; // the r-th set bit of dupM is the parent this slot clones
-                            for (int q = 0; q < r; ++q)
-                                m &= m - 1u;
-                            src = gbase + __ffs(m) - 1;
-                        }
+                        if (r < nd) // the r-th set bit of dupM is the parent this slot clones
+                            src = gbase + (int)__fns(dupM, 0u, r + 1);
                     }
                     if (__any_sync(FULL, src != lane)) {
                         const float pc1 = __shfl_sync(FULL, c1, src);
