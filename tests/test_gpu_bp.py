@@ -252,3 +252,15 @@ def test_kernel_variants_agree(kernel, tpf):
     nat.check(nat.load().pc_bp_decode(x.data_ptr(), 64, dc.ref, ctypes.byref(cfg), u.data_ptr(), None, None, None,
                                       it.data_ptr(), cv.data_ptr(), None, nat.stream_handle()), "bp")
     assert torch.equal(u, base.u_hat) and torch.equal(it, base.iterations_used)
+
+
+def test_crc24_stop_vs_oracle():
+    """The fused CRC stop with a 24-bit syndrome (polar.py:37-41)."""
+    code = CodeConfig(1024, 700, crc=24)
+    sigma = ebno_to_sigma(3.0, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(2424, 0, f))[1] for f in range(300)])
+    llrs = llrs.astype(np.float32).astype(np.float64)
+    ref_u, ref_it, ref_cv = oracle.bp_batch(llrs, code, stop_mode="crc")
+    got = bp_decode_batch(llrs, code, BpConfig(i_max=50, stop_mode="crc"))
+    late = _check_decisions("crc24", ref_u, ref_it, ref_cv, got, llrs, code)
+    print("near-tie frames:", late)

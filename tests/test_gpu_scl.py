@@ -139,3 +139,16 @@ def test_single_frame_api():
     bad[3] = np.inf
     with pytest.raises(ValueError):
         scl_decode(bad, code)
+
+
+@pytest.mark.parametrize("crc,L", [(24, 8), (8, 32)])
+def test_crc_widths_vs_oracle(crc, L):
+    """CRC-24 / CRC-8 codes (polar.py:37-41): the incremental syndrome of K3
+    against the oracle's CRC-aided winner rule."""
+    code = CodeConfig(1024, 700, crc=crc)
+    sigma = ebno_to_sigma(2.5, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(2400 + crc, L, f))[1] for f in range(150)])
+    llrs = llrs.astype(np.float32).astype(np.float64)
+    ref_u, ref_m, ref_ok = oracle.scl_batch(llrs, code, L)
+    got = scl_decode_batch(llrs, code, SclConfig(L))
+    _compare(f"crc{crc}L{L}", ref_u, ref_m, ref_ok, got)

@@ -227,3 +227,22 @@ def test_cli_parser_matches_reference_flags():
     assert cfg.ebno_points == (1.0, 2.5) and cfg.measure_time is False
     with pytest.raises(SystemExit):
         build_parser().parse_args(["--n", "8", "--k", "4", "--rate", "0.5", "--ebno", "1:2:1"])
+
+
+def test_scl_workspace_size_query_without_gpu():
+    """pc_scl_workspace_bytes sizes the K3 traceback from the code (no device
+    needed: it falls back to 148 SMs); bad configurations return -1."""
+    lib = nat.load()
+
+    def code_struct(N, k, crc=16):
+        return nat.PcCode(N, int(np.log2(N)), k, k - crc, crc, 0, 0, N - k, 1, 1, 1, 1, None)
+
+    small = lib.pc_scl_workspace_bytes(ctypes.byref(code_struct(1024, 512)), ctypes.byref(ps.SclConfig(32).native()))
+    large = lib.pc_scl_workspace_bytes(ctypes.byref(code_struct(4096, 2048)), ctypes.byref(ps.SclConfig(32).native()))
+    assert small > 256 and large > 256  # resident warps x windows x 160 B
+    bad = ps.SclConfig(32).native()
+    bad.L = 3
+    assert lib.pc_scl_workspace_bytes(ctypes.byref(code_struct(1024, 512)), ctypes.byref(bad)) == -1
+    # v2 (N < 32) needs only the counter block
+    assert lib.pc_scl_workspace_bytes(ctypes.byref(code_struct(16, 8, 0)), ctypes.byref(ps.SclConfig(4).native())) \
+        == lib.pc_workspace_bytes()
