@@ -42,12 +42,17 @@ N, K, LIST, IMAX = 1024, 512, 32, 50
 SEED = 20240917
 def mufu_per_alg_g(n: int, keep: bool) -> float:
     """MUFU ops K1 spends per ALGORITHMIC exact g (the reference's 2nN per
-    frame-iteration, bp.py:138-161).  A PE (two g) costs 7 MUFU (3 EX2 + 4 LG2,
-    bp_math.cuh); with the kept exponentials (N <= 2048) the L-sweep PEs at
-    boundaries 1..n-1 cost 6; R[n] (never read) is not computed."""
-    r = (n - 1) * 7
+    frame-iteration, bp.py:138-161).  A PE (two g) needs 3 exponentials and 4
+    logarithms (bp_math.cuh); the R sweep evaluates its sum operand's
+    exponential on the FMA pipe (ex2_fma), so an R-sweep PE costs 6 MUFU; an
+    L-sweep PE costs 7, or 6 with the kept exponentials (N <= 4096 at the
+    default threads per frame) at boundaries 1..n-1; R[n] (never read) is not
+    computed."""
+    r = (n - 1) * 6
     l_ = 7 + (n - 1) * (6 if keep else 7)
     return (r + l_) / 2 / (2 * n)  # per PE-pair of sweeps -> per g, over the 2n algorithmic g per node pair
+
+
 WORKLOAD = "hybrid BP->SCL N=1024 K=512 (496 payload + CRC-16) L=32 i_max=50, Eb/N0 1-4 dB step 0.5"
 
 

@@ -46,6 +46,15 @@ __host__ __device__ constexpr float bp_unit_in() { return GMODE == 0 ? PC_LOG2E 
 template <int GMODE>
 __host__ __device__ constexpr float bp_unit_out() { return GMODE == 0 ? PC_LN2 : 1.0f; }
 
+// The exponential of the PE's sum operand (l2 + r2) runs on the FMA pipe
+// (ex2_fma): the kernel is XU-bound with issue slots to spare.
+#ifndef BP_EX2_Y1
+#define BP_EX2_Y1 ex2_fma
+#endif
+#ifndef BP_EX2_Y1L
+#define BP_EX2_Y1L ex2_approx
+#endif
+
 // Core of a PE update with the three exponentials p = 2^-|v| given (GMODE 0).
 __device__ __forceinline__ void bp_pe2_core(float x, float y1, float y2, float px, float p1, float p2, float add,
                                             float lim, float &o1, float &o2)
@@ -74,7 +83,7 @@ __device__ __forceinline__ void bp_pe2(float x, float y1, float y2, float add, f
         return;
     }
     if (GMODE == 0) { // log2 units: p = 2^-|v'|
-        bp_pe2_core(x, y1, y2, ex2_approx(-fabsf(x)), ex2_approx(-fabsf(y1)), ex2_approx(-fabsf(y2)), add, lim, o1,
+        bp_pe2_core(x, y1, y2, ex2_approx(-fabsf(x)), BP_EX2_Y1(-fabsf(y1)), ex2_approx(-fabsf(y2)), add, lim, o1,
                     o2);
         return;
     }
@@ -92,14 +101,14 @@ __device__ __forceinline__ void bp_pe2_keep(float x, float y1, float y2, float a
                                             float &px)
 {
     px = ex2_approx(-fabsf(x));
-    bp_pe2_core(x, y1, y2, px, ex2_approx(-fabsf(y1)), ex2_approx(-fabsf(y2)), add, lim, o1, o2);
+    bp_pe2_core(x, y1, y2, px, BP_EX2_Y1(-fabsf(y1)), ex2_approx(-fabsf(y2)), add, lim, o1, o2);
 }
 
 // GMODE 0 L-sweep PE with p2 = 2^-|y2| supplied (y2 = a, kept from the R sweep).
 __device__ __forceinline__ void bp_pe2_p2(float x, float y1, float y2, float p2, float add, float lim, float &o1,
                                           float &o2)
 {
-    bp_pe2_core(x, y1, y2, ex2_approx(-fabsf(x)), ex2_approx(-fabsf(y1)), p2, add, lim, o1, o2);
+    bp_pe2_core(x, y1, y2, ex2_approx(-fabsf(x)), BP_EX2_Y1L(-fabsf(y1)), p2, add, lim, o1, o2);
 }
 
 } // namespace pc

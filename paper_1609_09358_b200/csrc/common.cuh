@@ -25,6 +25,22 @@ __device__ __forceinline__ float lg2_approx(float x)
     return y;
 }
 
+// 2^x for x in [-126, 0] on the FMA/ALU pipes (no MUFU): x = j + f with j the
+// nearest integer (magic-number rounding), f in [-0.5, 0.5]; degree-5
+// polynomial for 2^f (relative error < 2.2e-7 in fp32, the same order as
+// ex2.approx), then j added to the exponent field.
+__device__ __forceinline__ float ex2_fma(float x)
+{
+    const float t = __fadd_rn(x, 12582912.0f); // 1.5 * 2^23
+    const float f = __fsub_rn(x, __fsub_rn(t, 12582912.0f));
+    float p = fmaf(0.0013266970636323094f, f, 0.009675459936261177f);
+    p = fmaf(p, f, 0.05550742521882057f);
+    p = fmaf(p, f, 0.24022121727466583f);
+    p = fmaf(p, f, 0.6931469440460205f);
+    p = fmaf(p, f, 1.0000001192092896f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ uint64_t globaltimer()
 {
     uint64_t t;
