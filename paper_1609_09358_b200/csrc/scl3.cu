@@ -2,7 +2,6 @@
 #include "args.cuh"
 #include "scl3_decl.cuh"
 
-#include <cstdlib>
 
 namespace pc {
 
@@ -45,8 +44,9 @@ int scl3_prepare(SclArgs &a, int L, int nv_req)
     o += 128; // per group 4L words: candidate metrics + indices
     a.o_wrow = o;
     o += (F * W + 3) & ~3;
-    const char *env = getenv("PC_SCL_CH_SMEM"); // dev knob: channel LLRs staged in shared memory
-    const bool ch_smem = env != nullptr ? atoi(env) != 0 : false;
+    // Channel LLRs stay in global memory (L1/L2): staging them in shared memory
+    // costs a warp per SM and measured slower (tools/scl_ab.py, round 1).
+    const bool ch_smem = false;
     a.o_ch = ch_smem ? o : -1;
     if (ch_smem)
         o += F * a.code.N;
@@ -54,8 +54,7 @@ int scl3_prepare(SclArgs &a, int L, int nv_req)
     a.table_words = 0;
     // The frozen prefix is decoded element-parallel in the slots of lanes 1..31
     // (unused while one path is alive): two ping-pong buffers of N floats.
-    const char *envp = getenv("PC_SCL_PREFIX"); // dev knob
-    a.prefix = (L == 32 && 2 * a.code.N <= 31 * a.ss && (envp == nullptr || atoi(envp) != 0)) ? 1 : 0;
+    a.prefix = (L == 32 && 2 * a.code.N <= 31 * a.ss && a.code.first_info > 0) ? 1 : 0;
     return PC_OK;
 }
 
