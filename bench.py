@@ -160,10 +160,7 @@ def run_gpu(args):
     import torch
     import torch.distributed as dist
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch, dist, rank, world, local = _gpu_common(args)
 
     from paper_1609_09358_b200 import BpConfig, CodeConfig, HybridDecoder, SclConfig
     from paper_1609_09358_b200 import _native as nat
@@ -245,15 +242,17 @@ def run_gpu(args):
     torch.cuda.synchronize()
     if world > 1:  # whole-job statistics: sum the per-rank counters (off the timed path)
         stats = torch.tensor([[iters_sum[p], round(gammas[p] * B)] for p in range(len(EBNO))], dtype=torch.int64,
-                             device=dev)
+                             device=COMM)
         dist.all_reduce(stats)
-        dist.all_reduce(errs)
+        errs_c = errs.to(COMM)
+        dist.all_reduce(errs_c)
+        errs = errs_c.to(dev)
         for p in range(len(EBNO)):
             iters_sum[p] = int(stats[p, 0]) / world  # per-rank average keeps the per-GPU roofline arithmetic
             gammas[p] = float(stats[p, 1]) / (B * world)
     errs_h = errs.cpu().numpy()
 
-    max_ms = max_over_ranks(elapsed_ms, device=dev)
+    max_ms = max_over_ranks(elapsed_ms, device=COMM)
     bits_step = B * m * len(EBNO)
     value = world * bits_step * args.steps / (max_ms * 1e-3) / 1e9
 
@@ -306,7 +305,7 @@ def run_gpu(args):
         dec.decode_host_many(host * args.steps)
         barrier()
         e2e_s = time.perf_counter() - t0
-        e2e_val = world * bits_step * args.steps / max_over_ranks(e2e_s, device=dev) / 1e9
+        e2e_val = world * bits_step * args.steps / max_over_ranks(e2e_s, device=COMM) / 1e9
     h2d = B * N * 4 * len(EBNO)
     d2h = B * (MW * 4 + 1) * len(EBNO)
 
@@ -351,14 +350,28 @@ def run_gpu(args):
     return 0
 
 # ------------------------------------------------------ secondary workloads --
+COMM = None  # device of the collective tensors (the GPU under NCCL, the CPU under gloo)
+
+
 def _gpu_common(args):
+    """One process per GPU over NCCL.  When more ranks than GPUs are started
+    (a test of the multi-rank path on a smaller box) the ranks share GPUs and
+    the collectives run over gloo on CPU tensors."""
+    global COMM
     import torch
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    ngpu = torch.cuda.device_count()
+    local = local % max(1, ngpu)
     torch.cuda.set_device(local)
+    COMM = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if ngpu >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+            COMM = torch.device("cpu")
     return torch, dist, rank, world, local
 
 
@@ -439,7 +452,7 @@ def run_c4(args):
     torch.cuda.synchronize()
     it_sum = iters.to(torch.int64).sum(dim=1).cpu().numpy()
     errs_h = errs.cpu().numpy()
-    max_ms = max_over_ranks(ms, device=dev)
+    max_ms = max_over_ranks(ms, device=COMM)
     value = world * B * m * len(pts) * args.steps / (max_ms * 1e-3) / 1e9
     g_step = int(it_sum.sum()) * 2 * code.n * n4
     achieved = g_step / (sum(pt_ms) * 1e-3) / 1e9
@@ -488,7 +501,7 @@ def run_c4(args):
     te = time.perf_counter()
     e2e_run(args.steps)
     barrier()
-    e2e_val = world * B * m * len(pts) * args.steps / max_over_ranks(time.perf_counter() - te, device=dev) / 1e9
+    e2e_val = world * B * m * len(pts) * args.steps / max_over_ranks(time.perf_counter() - te, device=COMM) / 1e9
     if rank == 0:
         cpu = None
         if not args.no_cpu:
@@ -594,7 +607,7 @@ def run_c5(args):
                 dec(B)
             b.record()
             barrier()
-            ms = max_over_ranks(a.elapsed_time(b) / args.steps, device=dev)
+            ms = max_over_ranks(a.elapsed_time(b) / args.steps, device=COMM)
             total_ms += ms
             dec(B, stamp=True)
             nat.check(lib.pc_count_errors(pay.data_ptr(), msg.data_ptr(), B, m, errs[li].data_ptr(), st), "count")
