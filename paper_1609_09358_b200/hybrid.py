@@ -208,8 +208,8 @@ class HybridDecoder:
     def decode_host_many(self, batches):
         """End-to-end call over several HOST batches (pinned float32 [B_i, N]):
         the H2D copy of batch i+1 runs on a copy stream while batch i decodes
-        (two device input buffers), each batch's payload words and converged
-        flags are read back right after its decode.  Returns a list of
+        (two device input buffers), and each batch's payload words and converged
+        flags are read back on the copy stream while the next batch decodes.  Returns a list of
         (payload words uint32 [B_i, ceil(m/32)], converged bool [B_i]) numpy
         arrays, in order: views of pinned buffers that the next call reuses (copy
         them to keep them).  Results equal ``decode_host`` per batch."""
@@ -239,20 +239,37 @@ class HybridDecoder:
                 ev.record(self._s_copy)
             h2d[i] = ev
 
+        # Batches alternate between this decoder and a twin (same code and
+        # configuration, own result buffers), so the D2H copy of batch i runs on
+        # the copy stream while batch i+1 decodes.
+        if getattr(self, "_twin", None) is None:
+            self._twin = HybridDecoder(self.code, self.bp_cfg, self.scl_cfg, capacity=self.capacity,
+                                       chunk=self.chunk, overlap=self.overlap, device=self.device)
+        decs = (self, self._twin)
+        d2h = [None] * len(batches)
         issue_h2d(0)
         for i, b in enumerate(batches):
             if i + 1 < len(batches):
                 issue_h2d(i + 1)
             B = int(b.shape[0])
+            dec = decs[i % 2]
             cur.wait_event(h2d[i])
-            self.run(self._dbuf[i % 2][:B], B)
+            if i >= 2:  # batch i-2's results (same decoder) have been copied out
+                cur.wait_event(d2h[i - 2])
+            dec.run(self._dbuf[i % 2][:B], B)
             ev = torch.cuda.Event()
             ev.record(cur)
             done[i] = ev
             pay, conv = self._pinned_out(i, B)
-            pay.copy_(self.payload[:B], non_blocking=True)
-            conv.copy_(self.conv[:B], non_blocking=True)
+            with torch.cuda.stream(self._s_copy):
+                self._s_copy.wait_event(ev)
+                pay.copy_(dec.payload[:B], non_blocking=True)
+                conv.copy_(dec.conv[:B], non_blocking=True)
+                e2 = torch.cuda.Event()
+                e2.record(self._s_copy)
+            d2h[i] = e2
             outs.append((pay, conv))
+        self._s_copy.synchronize()
         cur.synchronize()
         return [(p.numpy().view(np.uint32), c.numpy().view(np.bool_)) for p, c in outs]
 
