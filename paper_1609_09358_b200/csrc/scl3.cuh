@@ -326,12 +326,14 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                 }
             }
             __syncwarp();
-            const uint32_t fzw = (__ldg(frzg + (i0 >> 5)) >> (i0 & 31)) & ((1u << BL) - 1u);
-            const uint32_t daw = damg != nullptr ? (__ldg(damg + (i0 >> 5)) >> (i0 & 31)) & ((1u << BL) - 1u) : 0u;
+            const uint32_t bmask = BL == 32 ? 0xffffffffu : ((1u << (BL & 31)) - 1u);
+            const uint32_t fzw = (__ldg(frzg + (i0 >> 5)) >> (i0 & 31)) & bmask;
+            const uint32_t daw = damg != nullptr ? (__ldg(damg + (i0 >> 5)) >> (i0 & 31)) & bmask : 0u;
 
             // ================= the block's leaves, registers only =================
-            static_assert(T == 3 || T == 4, "the leaf code below is written for 8- or 16-leaf blocks");
-            float l3[8], l2[4], l1[2]; // levels 3 (T = 4 only), 2, 1 of the block; level T is x
+            static_assert(T >= 3 && T <= 5, "the leaf code below is written for 8- to 32-leaf blocks");
+            // registers of the block's levels below T (level T is x); unused ones for small T
+            float l4[16], l3[8], l2[4], l1[2];
             uint32_t psr = 0;   // partial sums of levels < T: level s at bits [2^s - 1, 2^(s+1) - 1)
             uint32_t betaT = 0; // the block's codeword (2^T bits) after its last leaf
             // One copy of the leaf code for all leaves (runtime j, warp-uniform
@@ -353,15 +355,27 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                             for (int t = 0; t < 4; ++t)
                                 l2[t] = scl_g(L3[t], L3[t + 4], (psr >> (3 + t)) & 1u);
                         } else {
-                            if constexpr (T == 4) {
+                            if constexpr (T >= 4) {
+                                const float *L4 = (T == 4) ? x : l4;
                                 if (j & 8) {
 #pragma unroll
                                     for (int t = 0; t < 8; ++t)
-                                        l3[t] = scl_g(x[t], x[t + 8], (psr >> (7 + t)) & 1u);
+                                        l3[t] = scl_g(L4[t], L4[t + 8], (psr >> (7 + t)) & 1u);
                                 } else {
+                                    if constexpr (T >= 5) {
+                                        if (j & 16) {
+#pragma unroll
+                                            for (int t = 0; t < 16; ++t)
+                                                l4[t] = scl_g(x[t], x[t + 16], (psr >> (15 + t)) & 1u);
+                                        } else {
+#pragma unroll
+                                            for (int t = 0; t < 16; ++t)
+                                                l4[t] = scl_f<FEX>(x[t], x[t + 16]);
+                                        }
+                                    }
 #pragma unroll
                                     for (int t = 0; t < 8; ++t)
-                                        l3[t] = scl_f<FEX>(x[t], x[t + 8]);
+                                        l3[t] = scl_f<FEX>(L4[t], L4[t + 8]);
                                 }
                             }
 #pragma unroll
@@ -508,7 +522,12 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                             for (int t = 0; t < BL; ++t)
                                 x[t] = __shfl_sync(FULL, x[t], src);
                         }
-                        if (T == 4 && (j & 4) == 0) {
+                        if (T >= 5 && (j & 8) == 0) {
+#pragma unroll
+                            for (int t = 0; t < 16; ++t)
+                                l4[t] = __shfl_sync(FULL, l4[t], src);
+                        }
+                        if (T >= 4 && (j & 4) == 0) {
 #pragma unroll
                             for (int t = 0; t < 8; ++t)
                                 l3[t] = __shfl_sync(FULL, l3[t], src);
@@ -567,10 +586,19 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                                 if constexpr (T == 3) {
                                     betaT = Fw;
                                 } else {
-                                    if (j & 8)
-                                        betaT = (((psr >> 7) ^ Fw) & 255u) | (Fw << 8);
-                                    else
+                                    if (j & 8) {
+                                        Fw = (((psr >> 7) ^ Fw) & 255u) | (Fw << 8);
+                                        if constexpr (T == 4) {
+                                            betaT = Fw;
+                                        } else {
+                                            if (j & 16)
+                                                betaT = (((psr >> 15) ^ Fw) & 0xffffu) | (Fw << 16);
+                                            else
+                                                psr = (psr & ~(0xffffu << 15)) | (Fw << 15);
+                                        }
+                                    } else {
                                         psr = (psr & ~(255u << 7)) | (Fw << 7);
+                                    }
                                 }
                             } else {
                                 psr = (psr & ~(15u << 3)) | (Fw << 3);

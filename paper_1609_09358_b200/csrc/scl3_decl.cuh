@@ -5,9 +5,9 @@
 namespace pc {
 namespace s3 {
 #ifndef PC_SCL3_T
-#define PC_SCL3_T 4
+#define PC_SCL3_T 5
 #endif
-constexpr int T = PC_SCL3_T; // leaf-block level: 2^T leaves per block (3 or 4)
+constexpr int T = PC_SCL3_T; // leaf-block level: 2^T leaves per block (3..5; 5 measured best)
 constexpr int BL = 1 << T; // leaves per block
 // word offset of partial-sum level s (T <= s <= n-1) inside a slot
 __host__ __device__ __forceinline__ int pso(int s) { return s < 5 ? s - T : (5 - T) + (1 << (s - 5)) - 1; }
