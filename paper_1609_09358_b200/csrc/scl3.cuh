@@ -505,14 +505,25 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                     const uint32_t dupM = (__ballot_sync(FULL, act && k0 && k1) >> gbase) & gmask_lo;
                     const int nf = __popc(freeM), nd = __popc(dupM);
                     int src = lane;
+                    // the r-th free slot (freed lanes, then virgin lanes) clones the r-th
+                    // duplicating parent: parents post their lane in a rank table
+                    int *ptab = reinterpret_cast<int *>(cg);
+                    const bool anydup = __any_sync(FULL, nd > 0);
+                    if (anydup) {
+                        if (act && k0 && k1)
+                            ptab[__popc(dupM & ((1u << pl) - 1u))] = lane;
+                        __syncwarp();
+                    }
                     if (act && (k0 || k1)) {
                         u = k0 ? 0u : 1u;
                         metric = k0 ? c0 : c1;
                     } else {
                         const int r = act ? __popc(freeM & ((1u << pl) - 1u)) : nf + (pl - P);
-                        if (r < nd) // the r-th set bit of dupM is the parent this slot clones
-                            src = gbase + (int)__fns(dupM, 0u, r + 1);
+                        if (r < nd)
+                            src = ptab[r];
                     }
+                    if (anydup)
+                        __syncwarp();
                     if (__any_sync(FULL, src != lane)) {
                         const float pc1 = __shfl_sync(FULL, c1, src);
                         // eager copy of the still-readable register levels: level s+1 while
