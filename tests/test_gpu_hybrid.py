@@ -144,3 +144,23 @@ def test_host_buffer_pipeline_matches_device_run():
         dec.run(b.cuda(), b.shape[0]).sync()
         r = dec.host_results()
         assert np.array_equal(pay, r["payload"]) and np.array_equal(conv, r["converged"])
+
+
+def test_n4096_hybrid_vs_oracle():
+    """C4's code through the whole hybrid (K1 at N=4096, K3 at N=4096 L=32)."""
+    import torch
+
+    code = CodeConfig(4096, 2048, crc=16)
+    sigma = ebno_to_sigma(2.0, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(4097, 0, f))[1] for f in range(96)])
+    llrs = llrs.astype(np.float32).astype(np.float64)
+    pay, prov, iters = oracle.hybrid_batch(llrs, code, i_max=50, L=32)
+    dec = HybridDecoder(code, BpConfig(i_max=50), SclConfig(32), capacity=96, chunk=48)
+    dec.run(torch.from_numpy(llrs.astype(np.float32)).cuda()).sync()
+    r = dec.host_results()
+    got = nat.unpack_bits(r["payload"], code.message_len)
+    flips = np.flatnonzero(~r["converged"] != prov)
+    diff = np.flatnonzero((got != pay).any(axis=1))
+    assert (~r["converged"]).sum() > 0, "no frame reached the list decoder"
+    assert set(diff.tolist()) <= set(flips.tolist())
+    assert np.all(iters[flips] > 20) and flips.size <= 2
