@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
     // compile-time stage accessors (every loop below is fully unrolled, so the
     // register arrays are indexed with constants)
 #define PA(j, k) Pa[(((j) - 2) * (Q / 2) + (k)) * TPF + tid]
+#define PAP(j, p) Pa[((j) - 2) * (N / 2) + (p)] // shared-memory boundaries: indexed by PE
     const float pprior = GMODE == 0 ? ex2_approx(-lim) : 0.0f; // 2^-|R[0]| of a frozen node
 #define RGET(s, r) ((s) == 0 ? pri[r] : ((s) <= NREG ? Rr[(s) > 0 ? (s) - 1 : 0][r] : Rs[((s) - BW) * N + base + (r)]))
 #define LGET(s, r) ((s) <= NREG ? Lr[(s) > 0 ? (s) - 1 : 0][r] : Ls[((s) - BW) * N + base + (r)])
@@ -178,49 +179,144 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
             }
         }
         __syncthreads();
+        // Shared-memory boundaries in pairs (j, j+1): the four nodes b, b+h, b+2h,
+        // b+3h (h = 2^(j-1)) are closed under both boundaries, so one thread
+        // runs both PEs of j and then both of j+1 with one barrier per pair.
 #pragma unroll
-        for (int j = BW + 1; j <= LOGN - 1; ++j) { // shared-memory boundaries
+        for (int j = BW + 1; j <= LOGN - 1; j += (Q >= 4 ? 2 : 1)) {
             const int h = 1 << (j - 1);
             const float *Rp = Rs + (j - 1 - BW) * N;
             float *Rd = Rs + (j - BW) * N;
             const float *Lj = Ls + (j - BW) * N;
+            if (Q >= 4 && j + 1 <= LOGN - 1) { // (Q >= 4: a 4-node group per thread)
+                float *Rd2 = Rs + (j + 1 - BW) * N;
+                const float *Lj2 = Ls + (j + 1 - BW) * N;
 #pragma unroll
-            for (int q = 0; q < PPT; ++q) {
-                const int p = tid + q * TPF;
-                const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
-                const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
-                float o1, o2;
-                if (PAS) {
-                    float px;
-                    bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, o1, o2, px);
-                    PA(j, q) = px;
-                } else {
-                    bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                for (int q = 0; q < Q / 4; ++q) {
+                    const int g = tid + q * TPF;
+                    const int n0 = ((g >> (j - 1)) << (j + 1)) | (g & (h - 1));
+                    const int n1 = n0 + h, n2 = n0 + 2 * h, n3 = n0 + 3 * h;
+                    float o[4];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) { // boundary j: (n0, n1), (n2, n3)
+                        const int i1 = e ? n2 : n0, i2 = i1 + h;
+                        const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
+                        if (PAS) {
+                            float px;
+                            bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, o[2 * e], o[2 * e + 1], px);
+                            PAP(j, ((i1 >> j) << (j - 1)) | (i1 & (h - 1))) = px;
+                        } else {
+                            bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o[2 * e], o[2 * e + 1]);
+                        }
+                    }
+                    Rd[n0] = o[0];
+                    Rd[n1] = o[1];
+                    Rd[n2] = o[2];
+                    Rd[n3] = o[3];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) { // boundary j + 1: (n0, n2), (n1, n3)
+                        const int i1 = e ? n1 : n0, i2 = i1 + 2 * h;
+                        const float av = o[e], r2v = o[e + 2], l1 = Lj2[i1], l2 = Lj2[i2];
+                        float p1, p2;
+                        if (PAS) {
+                            float px;
+                            bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, p1, p2, px);
+                            PAP(j + 1, ((i1 >> (j + 1)) << j) | (i1 & (2 * h - 1))) = px;
+                        } else {
+                            bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, p1, p2);
+                        }
+                        Rd2[i1] = p1;
+                        Rd2[i2] = p2;
+                    }
                 }
-                Rd[i1] = o1;
-                Rd[i2] = o2;
+            } else {
+#pragma unroll
+                for (int q = 0; q < PPT; ++q) {
+                    const int p = tid + q * TPF;
+                    const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
+                    const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
+                    float o1, o2;
+                    if (PAS) {
+                        float px;
+                        bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, o1, o2, px);
+                        PAP(j, p) = px;
+                    } else {
+                        bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                    }
+                    Rd[i1] = o1;
+                    Rd[i2] = o2;
+                }
             }
             __syncthreads();
         }
         // ================= L sweep =================
+        // shared-memory boundaries top-down in pairs (j + 1, j), as in the R sweep
 #pragma unroll
-        for (int j = LOGN; j >= BW + 1; --j) {
-            const int h = 1 << (j - 1);
-            const float *Rp = Rs + (j - 1 - BW) * N;
-            const float *Lj = Ls + (j - BW) * N;
-            float *Ld = Ls + (j - 1 - BW) * N;
+        for (int jt = LOGN; jt >= BW + 1; jt -= (Q >= 4 ? 2 : 1)) {
+            if (Q >= 4 && jt - 1 >= BW + 1) {
+                const int j = jt - 1;
+                const int h = 1 << (j - 1);
+                const float *Rj = Rs + (j - BW) * N;      // R[j]   (a, r2 of boundary j + 1)
+                const float *Rp = Rs + (j - 1 - BW) * N;  // R[j-1] (a, r2 of boundary j)
+                const float *Lt = Ls + (j + 1 - BW) * N;  // L[j+1]
+                float *Lm = Ls + (j - BW) * N;            // L[j]
+                float *Ld = Ls + (j - 1 - BW) * N;        // L[j-1]
 #pragma unroll
-            for (int q = 0; q < PPT; ++q) {
-                const int p = tid + q * TPF;
-                const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
-                const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
-                float o1, o2;
-                if (PAS && j <= LOGN - 1)
-                    bp_pe2_p2(l1, l2 + r2v, av, PA(j, q), l2, lim, o1, o2);
-                else
-                    bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
-                Ld[i1] = o1;
-                Ld[i2] = o2;
+                for (int q = 0; q < Q / 4; ++q) {
+                    const int g = tid + q * TPF;
+                    const int n0 = ((g >> (j - 1)) << (j + 1)) | (g & (h - 1));
+                    const int n1 = n0 + h, n2 = n0 + 2 * h, n3 = n0 + 3 * h;
+                    float m[4]; // L[j] at n0..n3
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) { // boundary j + 1: (n0, n2), (n1, n3)
+                        const int i1 = e ? n1 : n0, i2 = i1 + 2 * h;
+                        const float av = Rj[i1], r2v = Rj[i2], l1 = Lt[i1], l2 = Lt[i2];
+                        float o1, o2;
+                        if (PAS && j + 1 <= LOGN - 1)
+                            bp_pe2_p2(l1, l2 + r2v, av, PAP(j + 1, ((i1 >> (j + 1)) << j) | (i1 & (2 * h - 1))), l2,
+                                      lim, o1, o2);
+                        else
+                            bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                        m[e] = o1;
+                        m[e + 2] = o2;
+                    }
+                    Lm[n0] = m[0];
+                    Lm[n1] = m[1];
+                    Lm[n2] = m[2];
+                    Lm[n3] = m[3];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) { // boundary j: (n0, n1), (n2, n3)
+                        const int i1 = e ? n2 : n0, i2 = i1 + h;
+                        const float av = Rp[i1], r2v = Rp[i2], l1 = m[2 * e], l2 = m[2 * e + 1];
+                        float o1, o2;
+                        if (PAS)
+                            bp_pe2_p2(l1, l2 + r2v, av, PAP(j, ((i1 >> j) << (j - 1)) | (i1 & (h - 1))), l2, lim, o1,
+                                      o2);
+                        else
+                            bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                        Ld[i1] = o1;
+                        Ld[i2] = o2;
+                    }
+                }
+            } else {
+                const int j = jt;
+                const int h = 1 << (j - 1);
+                const float *Rp = Rs + (j - 1 - BW) * N;
+                const float *Lj = Ls + (j - BW) * N;
+                float *Ld = Ls + (j - 1 - BW) * N;
+#pragma unroll
+                for (int q = 0; q < PPT; ++q) {
+                    const int p = tid + q * TPF;
+                    const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
+                    const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
+                    float o1, o2;
+                    if (PAS && j <= LOGN - 1)
+                        bp_pe2_p2(l1, l2 + r2v, av, PAP(j, p), l2, lim, o1, o2);
+                    else
+                        bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                    Ld[i1] = o1;
+                    Ld[i2] = o2;
+                }
             }
             __syncthreads();
         }
@@ -335,6 +431,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
 #undef RGET
 #undef LGET
 #undef PA
+#undef PAP
 
 static size_t bp2_smem_bytes(int logn, int tpf)
 {
