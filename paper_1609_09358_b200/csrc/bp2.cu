@@ -76,19 +76,27 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
     const float lim = a.llr_max * KIN; // messages in the kernel's units (bp_math.cuh)
     const int base = warp * 32 * Q + lane * Q;
 
+    // the frame's channel LLRs land in L[n] by a TMA bulk copy while the
+    // threads clear the message rows; then each thread scales and clips its part
+    __shared__ __align__(8) uint64_t ch_bar;
+    float *Lch = Ls + (NSL - 1) * N;
+    if (tid == 0) {
+        mbar_init(&ch_bar, 1);
+        tma_load_1d(Lch, a.llr + (size_t)f * N, N * sizeof(float), &ch_bar);
+    }
     for (int w = tid; w < NW; w += TPF)
         frz[w] = a.code.frozen_bits[w];
-    const float *x = a.llr + (size_t)f * N;
-    float *Lch = Ls + (NSL - 1) * N;
-    for (int i = 4 * tid; i < N; i += 4 * TPF) {
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(x + i));
-        *reinterpret_cast<float4 *>(Lch + i) = make_float4(clampf(v.x * KIN, lim), clampf(v.y * KIN, lim),
-                                                          clampf(v.z * KIN, lim), clampf(v.w * KIN, lim));
-    }
     for (int i = tid; i < NSR * N; i += TPF)
         Rs[i] = 0.0f;
     for (int i = tid; i < (NSL - 1) * N; i += TPF)
         Ls[i] = 0.0f;
+    __syncthreads(); // the barrier is initialised before anyone waits on it
+    mbar_wait(&ch_bar, 0);
+    for (int i = 4 * tid; i < N; i += 4 * TPF) {
+        const float4 v = *reinterpret_cast<const float4 *>(Lch + i);
+        *reinterpret_cast<float4 *>(Lch + i) = make_float4(clampf(v.x * KIN, lim), clampf(v.y * KIN, lim),
+                                                          clampf(v.z * KIN, lim), clampf(v.w * KIN, lim));
+    }
     float Rr[NREG][Q], Lr[NREG][Q];
 #pragma unroll
     for (int s = 0; s < NREG; ++s)

@@ -41,6 +41,38 @@ __device__ __forceinline__ float ex2_fma(float x)
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// 1-D TMA bulk copy (cp.async.bulk, SASS UBLKCP) global -> shared memory,
+// completing on an mbarrier: one elected thread arms the barrier with the byte
+// count and issues the copy; every thread then waits on the barrier's phase.
+// dst / src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void mbar_init(uint64_t *mbar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(mbar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *mbar)
+{
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(mbar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase)
+{
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(mbar);
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "WAIT%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT%=;\n}" ::"r"(b),
+                 "r"(phase)
+                 : "memory");
+}
+
 __device__ __forceinline__ uint64_t globaltimer()
 {
     uint64_t t;
