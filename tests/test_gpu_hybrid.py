@@ -164,3 +164,57 @@ def test_n4096_hybrid_vs_oracle():
     assert (~r["converged"]).sum() > 0, "no frame reached the list decoder"
     assert set(diff.tolist()) <= set(flips.tolist())
     assert np.all(iters[flips] > 20) and flips.size <= 2
+
+
+def test_results_do_not_depend_on_chunking():
+    """Per-frame outputs are independent of the chunk size (ragged last chunk,
+    per-chunk queues and counters) and of the stream overlap."""
+    import torch
+
+    code = CodeConfig(1024, 512, crc=16)
+    sigma = ebno_to_sigma(1.5, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(77, 0, f))[1] for f in range(1000)])
+    x = torch.from_numpy(llrs.astype(np.float32)).cuda()
+    ref = None
+    for chunk, overlap in ((1000, True), (333, True), (100, False), (1, True)):
+        dec = HybridDecoder(code, BpConfig(i_max=50), SclConfig(32), capacity=1000, chunk=chunk, overlap=overlap)
+        dec.run(x).sync()
+        r = dec.host_results()
+        assert r["counts"].sum() == (~r["converged"]).sum()
+        if ref is None:
+            ref = r
+        else:
+            assert np.array_equal(r["payload"], ref["payload"]) and np.array_equal(r["converged"], ref["converged"])
+            assert np.array_equal(r["iters"], ref["iters"])
+
+
+def test_scl_queue_subset_and_empty_queue():
+    """K3 decodes exactly the queued frames (others untouched) and a zero-length
+    queue launches nothing."""
+    import ctypes
+    import torch
+
+    code = CodeConfig(1024, 512, crc=16)
+    sigma = ebno_to_sigma(1.5, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(78, 0, f))[1] for f in range(64)])
+    x = torch.from_numpy(llrs.astype(np.float32)).cuda()
+    from paper_1609_09358_b200 import scl_decode_batch
+
+    full = scl_decode_batch(x, code, SclConfig(32), payload=True)
+    lib = nat.load()
+    dc = nat.device_code(code)
+    cfg = SclConfig(32).native()
+    MW = (code.message_len + 31) // 32
+    for q in ([5, 17, 40, 63], []):
+        queue = torch.tensor(q + [0], dtype=torch.int32, device="cuda")
+        count = torch.tensor([len(q)], dtype=torch.int32, device="cuda")
+        pay = torch.full((64, MW), -1, dtype=torch.int32, device="cuda")
+        nat.check(lib.pc_scl_decode(x.data_ptr(), 64, queue.data_ptr(), count.data_ptr(), dc.ref, ctypes.byref(cfg),
+                                    None, pay.data_ptr(), None, None, None, None,
+                                    dc.scl_workspace(cfg).data_ptr(), nat.stream_handle()), "scl")
+        p = pay.cpu().numpy()
+        for f in range(64):
+            if f in q:
+                assert np.array_equal(p[f], full.payload_words[f].cpu().numpy())
+            else:
+                assert np.all(p[f] == -1)
