@@ -86,8 +86,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
     }
     for (int w = tid; w < NW; w += TPF)
         frz[w] = a.code.frozen_bits[w];
-    for (int i = tid; i < NSR * N; i += TPF)
-        Rs[i] = 0.0f;
+    // (the R rows are written by the R sweep before any read; only L starts at 0)
     for (int i = tid; i < (NSL - 1) * N; i += TPF)
         Ls[i] = 0.0f;
     __syncthreads(); // the barrier is initialised before anyone waits on it
@@ -418,20 +417,20 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 make_float2(su[r] * KOUT, su[r + 1] * KOUT);
     }
     __syncthreads();
+    // bit-pack with warp ballots: thread b of the pass owns bit b (coalesced
+    // info_pos reads, one store per 32 bits)
     if (a.u_bits != nullptr)
-        for (int w = tid; w < NW; w += TPF) {
-            uint32_t v = 0;
-            for (int b = 0; b < 32; ++b)
-                v |= (uint32_t)ub[32 * w + b] << b;
-            a.u_bits[(size_t)f * NW + w] = v;
+        for (int b = tid; b < 32 * NW; b += TPF) {
+            const uint32_t v = __ballot_sync(0xffffffffu, b < N && ub[b]);
+            if ((b & 31) == 0)
+                a.u_bits[(size_t)f * NW + (b >> 5)] = v;
         }
     if (a.payload != nullptr) {
-        const int MW = (a.code.m + 31) >> 5;
-        for (int w = tid; w < MW; w += TPF) {
-            uint32_t v = 0;
-            for (int b = 0; b < 32 && 32 * w + b < a.code.m; ++b)
-                v |= (uint32_t)ub[__ldg(a.code.info_pos + 32 * w + b)] << b;
-            a.payload[(size_t)f * MW + w] = v;
+        const int m = a.code.m, MW = (m + 31) >> 5;
+        for (int b = tid; b < 32 * MW; b += TPF) {
+            const uint32_t v = __ballot_sync(0xffffffffu, b < m && ub[__ldg(a.code.info_pos + b)]);
+            if ((b & 31) == 0)
+                a.payload[(size_t)f * MW + (b >> 5)] = v;
         }
     }
 }
