@@ -1,6 +1,5 @@
 """Encoder / CRC / generator / compaction kernels: bit-exact contracts."""
 
-import ctypes
 
 import numpy as np
 import pytest

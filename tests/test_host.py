@@ -5,7 +5,6 @@ import binascii
 import ctypes
 import math
 import re
-from pathlib import Path
 
 import numpy as np
 import pytest

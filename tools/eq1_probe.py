@@ -5,7 +5,6 @@ test 08, test_acceptance.py:258-284, for its CPU pipeline).
     python tools/eq1_probe.py
 """
 import sys; sys.path.insert(0,'.')
-import numpy as np
 from paper_1609_09358_b200 import BpConfig, CodeConfig, SclConfig, FrameJob, hybrid_decode_batch
 from paper_1609_09358_b200.channel import ebno_to_sigma, frame_rng, make_frame
 code = CodeConfig(1024, 512, crc=16)
