@@ -401,6 +401,13 @@ __global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
                     u = (dz && lam < 0.0f) ? 1u : 0u;
                     if (act)
                         metric += u ? inc1 : inc0;
+                } else if constexpr (L == 1) {
+                    // SC (one path per frame): keep the better child, a tie keeps u = 0
+                    // (candidate index 0 < 1, _kernels.py:253-267); no slot moves
+                    const float c0 = metric + inc0, c1 = metric + inc1;
+                    u = c1 < c0 ? 1u : 0u;
+                    if (act)
+                        metric = u ? c1 : c0;
                 } else {
                     const float c0 = act ? metric + inc0 : INFINITY;
                     const float c1 = act ? metric + inc1 : INFINITY;
