@@ -77,7 +77,9 @@ def test_virtual_levels_do_not_change_results(nv):
 
 
 @pytest.mark.parametrize("N,k,L,eb,count", [(1024, 512, 32, 1.5, 400), (1024, 512, 4, 1.0, 400),
-                                            (2048, 1024, 16, 2.0, 100), (64, 32, 2, 1.0, 400)])
+                                            (2048, 1024, 16, 2.0, 100), (64, 32, 2, 1.0, 400),
+                                            (2048, 1024, 32, 1.5, 300), (2048, 1024, 1, 2.0, 1000),
+                                            (4096, 2048, 32, 1.5, 48)])
 def test_winners_vs_oracle_at_scale(N, k, L, eb, count):
     code = CodeConfig(N, k, crc=16)
     sigma = ebno_to_sigma(eb, code.rate)
