@@ -44,9 +44,9 @@ __device__ __forceinline__ void bp_pe(int j, int p, const float *__restrict__ Rp
     }
     const float l1 = Lj[i1], l2 = Lj[i2];
     if (RSWEEP)
-        bp_pe2<GMODE>(av, l2 + r2, l1, r2, lim, o1, o2);
+        bp_pe2<GMODE, true>(av, l2 + r2, l1, r2, lim, o1, o2);
     else
-        bp_pe2<GMODE>(l1, l2 + r2, av, l2, lim, o1, o2);
+        bp_pe2<GMODE, false>(l1, l2 + r2, av, l2, lim, o1, o2);
 }
 
 template <int LOGN>
@@ -267,7 +267,7 @@ __global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float lim)
             const float av = R[(j - 1) * N + i1], r2 = R[(j - 1) * N + i2];
             const float l1 = L[j * N + i1], l2 = L[j * N + i2];
             float o1, o2;
-            bp_pe2<GMODE>(av, l2 + r2, l1, r2, lim, o1, o2);
+            bp_pe2<GMODE, true>(av, l2 + r2, l1, r2, lim, o1, o2);
             R[j * N + i1] = o1;
             R[j * N + i2] = o2;
         }
@@ -280,7 +280,7 @@ __global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float lim)
             const float av = R[(j - 1) * N + i1], r2 = R[(j - 1) * N + i2];
             const float l1 = L[j * N + i1], l2 = L[j * N + i2];
             float o1, o2;
-            bp_pe2<GMODE>(l1, l2 + r2, av, l2, lim, o1, o2);
+            bp_pe2<GMODE, false>(l1, l2 + r2, av, l2, lim, o1, o2);
             L[(j - 1) * N + i1] = o1;
             L[(j - 1) * N + i2] = o2;
         }

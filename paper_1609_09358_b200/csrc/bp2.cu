@@ -40,10 +40,17 @@ __host__ __device__ constexpr int bp2_base_bytes(int logn, int tpf)
     // R rows bw..n-1 and L rows bw..n (bw = log2 Q + 5, i.e. n - bw = log2 TPF - 5), plus N bytes of decisions
     return (2 * (ilog2c(tpf) - 5) + 1) * (1 << logn) * 4 + (1 << logn);
 }
-__host__ __device__ constexpr int bp2_pas_bytes(int logn, int tpf) { return (logn - 2) * ((1 << logn) / tpf / 2) * tpf * 4; }
-__host__ __device__ constexpr bool bp2_pas(int logn, int tpf, int gmode)
+// Boundaries 2..n-1 keep their exponentials when all of them (N/2 floats
+// each) fit beside the message rows in 225 KB of shared memory.  (Keeping only
+// the lower ones at N = 4096 measured 2-4% slower than keeping none:
+// tools/bp_tpf_probe.py.)  The KEPT(j) logic supports any prefix count.
+__host__ __device__ constexpr int bp2_keep(int logn, int tpf, int gmode)
 {
-    return gmode == 0 && bp2_base_bytes(logn, tpf) + bp2_pas_bytes(logn, tpf) <= 225 * 1024;
+    return gmode == 0 && bp2_base_bytes(logn, tpf) + (logn - 2) * (1 << logn) * 2 <= 225 * 1024 ? logn - 2 : 0;
+}
+__host__ __device__ constexpr int bp2_keep_bytes(int logn, int tpf, int gmode)
+{
+    return bp2_keep(logn, tpf, gmode) * (1 << logn) * 2;
 }
 
 template <int LOGN, int TPF, int GMODE>
@@ -65,7 +72,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
     float *Rs = sm;           // R[BW + r], r < NSR
     float *Ls = sm + NSR * N; // L[BW + r], r < NSL
     uint8_t *ub = reinterpret_cast<uint8_t *>(Ls + NSL * N);
-    constexpr bool PAS = bp2_pas(LOGN, TPF, GMODE);
+    constexpr int KEEP = bp2_keep(LOGN, TPF, GMODE);
     float *Pa = Ls + NSL * N + N / 4; // kept exponentials, [(j - 2) * Q/2 + k][tid]
     __shared__ uint32_t frz[NW];
     __shared__ uint32_t red[NWARP];
@@ -115,6 +122,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
 
     // compile-time stage accessors (every loop below is fully unrolled, so the
     // register arrays are indexed with constants)
+#define KEPT(j) ((j) >= 2 && (j) - 2 < KEEP)
 #define PA(j, k) Pa[(((j) - 2) * (Q / 2) + (k)) * TPF + tid]
 #define PAP(j, p) Pa[((j) - 2) * (N / 2) + (p)] // shared-memory boundaries: indexed by PE
     const float pprior = GMODE == 0 ? ex2_approx(-lim) : 0.0f; // 2^-|R[0]| of a frozen node
@@ -136,12 +144,12 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                     continue;
                 const int r2 = r1 + h;
                 const float av = RGET(j - 1, r1), r2v = RGET(j - 1, r2), l1 = LGET(j, r1), l2 = LGET(j, r2);
-                if (PAS && j >= 2) {
+                if (KEPT(j)) {
                     float px;
                     bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, Rr[j - 1][r1], Rr[j - 1][r2], px);
                     PA(j, ((r1 >> j) << (j - 1)) | (r1 & (h - 1))) = px;
                 } else {
-                    bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, Rr[j - 1][r1], Rr[j - 1][r2]);
+                    bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, Rr[j - 1][r1], Rr[j - 1][r2]);
                 }
             }
         }
@@ -166,12 +174,12 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 // (a, r2, l1, l2) of the PE at my node
                 const float av = hi ? pr : myR, r2v = hi ? myR : pr, l1 = hi ? pl : myL, l2 = hi ? myL : pl;
                 float o1, o2;
-                if (PAS) {
+                if (KEPT(j)) {
                     float px;
                     bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, o1, o2, px);
                     PA(j, k) = px;
                 } else {
-                    bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                    bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, o1, o2);
                 }
                 const float back = __shfl_xor_sync(0xffffffffu, hi ? o1 : o2, msk); // my output the partner computed
                 Rn[k] = hi ? back : o1;
@@ -208,12 +216,12 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                     for (int e = 0; e < 2; ++e) { // boundary j: (n0, n1), (n2, n3)
                         const int i1 = e ? n2 : n0, i2 = i1 + h;
                         const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
-                        if (PAS) {
+                        if (KEPT(j)) {
                             float px;
                             bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, o[2 * e], o[2 * e + 1], px);
                             PAP(j, ((i1 >> j) << (j - 1)) | (i1 & (h - 1))) = px;
                         } else {
-                            bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o[2 * e], o[2 * e + 1]);
+                            bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, o[2 * e], o[2 * e + 1]);
                         }
                     }
                     Rd[n0] = o[0];
@@ -225,12 +233,12 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                         const int i1 = e ? n1 : n0, i2 = i1 + 2 * h;
                         const float av = o[e], r2v = o[e + 2], l1 = Lj2[i1], l2 = Lj2[i2];
                         float p1, p2;
-                        if (PAS) {
+                        if (KEPT(j + 1)) {
                             float px;
                             bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, p1, p2, px);
                             PAP(j + 1, ((i1 >> (j + 1)) << j) | (i1 & (2 * h - 1))) = px;
                         } else {
-                            bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, p1, p2);
+                            bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, p1, p2);
                         }
                         Rd2[i1] = p1;
                         Rd2[i2] = p2;
@@ -243,12 +251,12 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                     const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
                     const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
                     float o1, o2;
-                    if (PAS) {
+                    if (KEPT(j)) {
                         float px;
                         bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, o1, o2, px);
                         PAP(j, p) = px;
                     } else {
-                        bp_pe2<GMODE>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                        bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, o1, o2);
                     }
                     Rd[i1] = o1;
                     Rd[i2] = o2;
@@ -279,11 +287,11 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                         const int i1 = e ? n1 : n0, i2 = i1 + 2 * h;
                         const float av = Rj[i1], r2v = Rj[i2], l1 = Lt[i1], l2 = Lt[i2];
                         float o1, o2;
-                        if (PAS && j + 1 <= LOGN - 1)
+                        if (KEPT(j + 1))
                             bp_pe2_p2(l1, l2 + r2v, av, PAP(j + 1, ((i1 >> (j + 1)) << j) | (i1 & (2 * h - 1))), l2,
                                       lim, o1, o2);
                         else
-                            bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                            bp_pe2<GMODE, false>(l1, l2 + r2v, av, l2, lim, o1, o2);
                         m[e] = o1;
                         m[e + 2] = o2;
                     }
@@ -296,11 +304,11 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                         const int i1 = e ? n2 : n0, i2 = i1 + h;
                         const float av = Rp[i1], r2v = Rp[i2], l1 = m[2 * e], l2 = m[2 * e + 1];
                         float o1, o2;
-                        if (PAS)
+                        if (KEPT(j))
                             bp_pe2_p2(l1, l2 + r2v, av, PAP(j, ((i1 >> j) << (j - 1)) | (i1 & (h - 1))), l2, lim, o1,
                                       o2);
                         else
-                            bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                            bp_pe2<GMODE, false>(l1, l2 + r2v, av, l2, lim, o1, o2);
                         Ld[i1] = o1;
                         Ld[i2] = o2;
                     }
@@ -317,10 +325,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                     const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1)), i2 = i1 + h;
                     const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
                     float o1, o2;
-                    if (PAS && j <= LOGN - 1)
+                    if (KEPT(j))
                         bp_pe2_p2(l1, l2 + r2v, av, PAP(j, p), l2, lim, o1, o2);
                     else
-                        bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                        bp_pe2<GMODE, false>(l1, l2 + r2v, av, l2, lim, o1, o2);
                     Ld[i1] = o1;
                     Ld[i2] = o2;
                 }
@@ -343,10 +351,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 // (a, r2, l1, l2) of the PE at my node
                 const float av = hi ? pr : myR, r2v = hi ? myR : pr, l1 = hi ? pl : myL, l2 = hi ? myL : pl;
                 float o1, o2;
-                if (PAS && j <= LOGN - 1)
+                if (KEPT(j))
                     bp_pe2_p2(l1, l2 + r2v, av, PA(j, k), l2, lim, o1, o2);
                 else
-                    bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                    bp_pe2<GMODE, false>(l1, l2 + r2v, av, l2, lim, o1, o2);
                 const float back = __shfl_xor_sync(0xffffffffu, hi ? o1 : o2, msk); // my output the partner computed
                 Ln[k] = hi ? back : o1;
                 Ln[k + Q / 2] = hi ? o2 : back;
@@ -365,12 +373,12 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 const int r2 = r1 + h;
                 const float av = RGET(j - 1, r1), r2v = RGET(j - 1, r2), l1 = LGET(j, r1), l2 = LGET(j, r2);
                 float o1, o2;
-                if (PAS && j >= 2)
+                if (KEPT(j))
                     bp_pe2_p2(l1, l2 + r2v, av, PA(j, ((r1 >> j) << (j - 1)) | (r1 & (h - 1))), l2, lim, o1, o2);
-                else if (PAS)
+                else if (GMODE == 0 && j == 1)
                     bp_pe2_p2(l1, l2 + r2v, av, av != 0.0f ? pprior : 1.0f, l2, lim, o1, o2); // R[0] prior
                 else
-                    bp_pe2<GMODE>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                    bp_pe2<GMODE, false>(l1, l2 + r2v, av, l2, lim, o1, o2);
                 if (j > 1) {
                     Lr[j - 2][r1] = o1;
                     Lr[j - 2][r2] = o2;
@@ -439,6 +447,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
 #undef LGET
 #undef PA
 #undef PAP
+#undef KEPT
 
 static size_t bp2_smem_bytes(int logn, int tpf)
 {
@@ -454,7 +463,7 @@ template <int LOGN, int TPF, int GMODE>
 static int launch_bp2_t(const BpArgs &a, cudaStream_t s)
 {
     auto kern = k_bp2<LOGN, TPF, GMODE>;
-    const size_t smem = bp2_smem_bytes(LOGN, TPF) + (bp2_pas(LOGN, TPF, GMODE) ? bp2_pas_bytes(LOGN, TPF) : 0);
+    const size_t smem = bp2_smem_bytes(LOGN, TPF) + bp2_keep_bytes(LOGN, TPF, GMODE);
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return PC_ERR_CUDA;

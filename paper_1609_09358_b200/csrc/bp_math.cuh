@@ -74,7 +74,10 @@ __device__ __forceinline__ void bp_pe2_core(float x, float y1, float y2, float p
     o2 = clampf(g2 + add, lim);
 }
 
-template <int GMODE>
+// RS: an R-sweep PE (the sum operand's exponential on the FMA pipe) or an
+// L-sweep PE (on the MUFU) -- the same choice as bp_pe2_keep / bp_pe2_p2, so a
+// PE's arithmetic never depends on which boundaries keep their exponentials.
+template <int GMODE, bool RS>
 __device__ __forceinline__ void bp_pe2(float x, float y1, float y2, float add, float lim, float &o1, float &o2)
 {
     if (GMODE == 2) {
@@ -83,8 +86,8 @@ __device__ __forceinline__ void bp_pe2(float x, float y1, float y2, float add, f
         return;
     }
     if (GMODE == 0) { // log2 units: p = 2^-|v'|
-        bp_pe2_core(x, y1, y2, ex2_approx(-fabsf(x)), BP_EX2_Y1(-fabsf(y1)), ex2_approx(-fabsf(y2)), add, lim, o1,
-                    o2);
+        bp_pe2_core(x, y1, y2, ex2_approx(-fabsf(x)), RS ? BP_EX2_Y1(-fabsf(y1)) : BP_EX2_Y1L(-fabsf(y1)),
+                    ex2_approx(-fabsf(y2)), add, lim, o1, o2);
         return;
     }
     const float ax = fabsf(x), a1 = fabsf(y1), a2 = fabsf(y2);
