@@ -43,13 +43,14 @@ SEED = 20240917
 def mufu_per_alg_g(n: int, keep: bool) -> float:
     """MUFU ops K1 spends per ALGORITHMIC exact g (the reference's 2nN per
     frame-iteration, bp.py:138-161).  A PE (two g) needs 3 exponentials and 4
-    logarithms (bp_math.cuh); the R sweep evaluates its sum operand's
-    exponential on the FMA pipe (ex2_fma), so an R-sweep PE costs 6 MUFU; an
-    L-sweep PE costs 7, or 6 with the kept exponentials (N <= 4096 at the
-    default threads per frame) at boundaries 1..n-1; R[n] (never read) is not
+    logarithms (bp_math.cuh).  The R sweep evaluates its sum operand's
+    exponential on the FMA pipe (ex2_fma): 6 MUFU per R-sweep PE.  With kept
+    exponentials (N <= 2048) an L-sweep PE at boundaries 1..n-1 reuses the R
+    sweep's 2^-|a| (6 MUFU; 7 at boundary n); without them (N = 4096) the L
+    sweep also uses ex2_fma (6 MUFU everywhere).  R[n] (never read) is not
     computed."""
     r = (n - 1) * 6
-    l_ = 7 + (n - 1) * (6 if keep else 7)
+    l_ = 7 + (n - 1) * 6 if keep else 6 * n
     return (r + l_) / 2 / (2 * n)  # per PE-pair of sweeps -> per g, over the 2n algorithmic g per node pair
 
 
@@ -456,7 +457,7 @@ def run_c4(args):
     value = world * B * m * len(pts) * args.steps / (max_ms * 1e-3) / 1e9
     g_step = int(it_sum.sum()) * 2 * code.n * n4
     achieved = g_step / (sum(pt_ms) * 1e-3) / 1e9
-    peak = _xu_peak_gg(torch, dev, mufu_per_alg_g(code.n, False))  # N = 4096: no kept exponentials (no room)
+    peak = _xu_peak_gg(torch, dev, mufu_per_alg_g(code.n, False))  # N = 4096: no kept exponentials, FMA exp2 in both sweeps
     # e2e: pinned host LLRs -> device, decode, payload + flags -> host, every step
     host = [torch.empty((B, n4), dtype=torch.float32, pin_memory=True) for _ in pts]
     for p in range(len(pts)):

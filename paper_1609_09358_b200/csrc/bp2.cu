@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                             bp_pe2_p2(l1, l2 + r2v, av, PAP(j + 1, ((i1 >> (j + 1)) << j) | (i1 & (2 * h - 1))), l2,
                                       lim, o1, o2);
                         else
-                            bp_pe2<GMODE, false>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                            bp_pe2<GMODE, false, KEEP == 0 && GMODE == 0>(l1, l2 + r2v, av, l2, lim, o1, o2);
                         m[e] = o1;
                         m[e + 2] = o2;
                     }
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                             bp_pe2_p2(l1, l2 + r2v, av, PAP(j, ((i1 >> j) << (j - 1)) | (i1 & (h - 1))), l2, lim, o1,
                                       o2);
                         else
-                            bp_pe2<GMODE, false>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                            bp_pe2<GMODE, false, KEEP == 0 && GMODE == 0>(l1, l2 + r2v, av, l2, lim, o1, o2);
                         Ld[i1] = o1;
                         Ld[i2] = o2;
                     }
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                     if (KEPT(j))
                         bp_pe2_p2(l1, l2 + r2v, av, PAP(j, p), l2, lim, o1, o2);
                     else
-                        bp_pe2<GMODE, false>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                        bp_pe2<GMODE, false, KEEP == 0 && GMODE == 0>(l1, l2 + r2v, av, l2, lim, o1, o2);
                     Ld[i1] = o1;
                     Ld[i2] = o2;
                 }
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 if (KEPT(j))
                     bp_pe2_p2(l1, l2 + r2v, av, PA(j, k), l2, lim, o1, o2);
                 else
-                    bp_pe2<GMODE, false>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                    bp_pe2<GMODE, false, KEEP == 0 && GMODE == 0>(l1, l2 + r2v, av, l2, lim, o1, o2);
                 const float back = __shfl_xor_sync(0xffffffffu, hi ? o1 : o2, msk); // my output the partner computed
                 Ln[k] = hi ? back : o1;
                 Ln[k + Q / 2] = hi ? o2 : back;
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 else if (GMODE == 0 && j == 1)
                     bp_pe2_p2(l1, l2 + r2v, av, av != 0.0f ? pprior : 1.0f, l2, lim, o1, o2); // R[0] prior
                 else
-                    bp_pe2<GMODE, false>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                    bp_pe2<GMODE, false, KEEP == 0 && GMODE == 0>(l1, l2 + r2v, av, l2, lim, o1, o2);
                 if (j > 1) {
                     Lr[j - 2][r1] = o1;
                     Lr[j - 2][r2] = o2;

@@ -77,7 +77,9 @@ __device__ __forceinline__ void bp_pe2_core(float x, float y1, float y2, float p
 // RS: an R-sweep PE (the sum operand's exponential on the FMA pipe) or an
 // L-sweep PE (on the MUFU) -- the same choice as bp_pe2_keep / bp_pe2_p2, so a
 // PE's arithmetic never depends on which boundaries keep their exponentials.
-template <int GMODE, bool RS>
+// LFMA: the L sweep also uses the FMA pipe (kernels without kept exponentials,
+// N = 4096, where the MUFU has one more op per L-sweep PE to shed).
+template <int GMODE, bool RS, bool LFMA = false>
 __device__ __forceinline__ void bp_pe2(float x, float y1, float y2, float add, float lim, float &o1, float &o2)
 {
     if (GMODE == 2) {
@@ -86,8 +88,9 @@ __device__ __forceinline__ void bp_pe2(float x, float y1, float y2, float add, f
         return;
     }
     if (GMODE == 0) { // log2 units: p = 2^-|v'|
-        bp_pe2_core(x, y1, y2, ex2_approx(-fabsf(x)), RS ? BP_EX2_Y1(-fabsf(y1)) : BP_EX2_Y1L(-fabsf(y1)),
-                    ex2_approx(-fabsf(y2)), add, lim, o1, o2);
+        bp_pe2_core(x, y1, y2, ex2_approx(-fabsf(x)),
+                    (RS || LFMA) ? BP_EX2_Y1(-fabsf(y1)) : BP_EX2_Y1L(-fabsf(y1)), ex2_approx(-fabsf(y2)), add, lim,
+                    o1, o2);
         return;
     }
     const float ax = fabsf(x), a1 = fabsf(y1), a2 = fabsf(y2);
