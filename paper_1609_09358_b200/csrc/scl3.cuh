@@ -2,26 +2,31 @@
 //
 // Same decoder as scl.cu (reference _kernels.py:144-333 + scl.py:177-191, with
 // the reference's logical slot numbering and (metric, candidate index) order),
-// restructured around blocks of 2^T = 8 leaves:
+// restructured around blocks of 2^T = 32 leaves (T = PC_SCL3_T, scl3_decl.cuh):
 //
 //   * upper descent, once per block: tree levels >= T+1 live in shared memory
 //     with lazy slot pointers (as in v2) and produce the block's level-T LLRs
 //     straight into registers;
-//   * the 8 leaves of a block run fully unrolled on registers: levels 0..T-1,
-//     the partial sums of those levels (one word) and all per-leaf control are
-//     compile-time.  A clone copies the parent's still-readable register
-//     levels with shuffles (the reference's eager copy, _kernels.py:288-303);
-//   * survivor selection at a full list (P == L): the agreeing children start
-//     as survivors and the best excluded candidate is swapped for the worst
-//     kept one until no excluded candidate beats a kept one.  Each round is
-//     two warp reductions (redux.sync at L = 32); the common reliable position
-//     exits after the first round.  The result is exactly the L smallest
-//     (metric, index) pairs (_kernels.py:253-267);
+//   * the leaves of a block run on registers only: levels 0..T-1, the partial
+//     sums of those levels (one word) and the per-leaf control.  One copy of
+//     the leaf code serves every leaf (runtime leaf index, warp-uniform
+//     branches) -- an unrolled block overflows the instruction cache.  A clone
+//     copies the parent's still-readable register levels with shuffles (the
+//     reference's eager copy, _kernels.py:288-303);
+//   * survivor selection at a full list (P == L): every agreeing child below
+//     the best disagreeing one is kept and every disagreeing child above the
+//     worst agreeing one dropped (two warp reductions, redux.sync at L = 32);
+//     the remaining slots go to the smallest of the uncertain set, ranked in
+//     shared memory.  The result is exactly the L smallest (metric, index)
+//     pairs (_kernels.py:253-267);
+//   * the frozen prefix (one path, all decisions 0) is decoded element-parallel
+//     by the whole warp (frozen_prefix) with bit-identical state;
 //   * the CRC syndrome of every path is carried incrementally (one XOR of the
 //     position's syndrome column per decided 1) and copied on clone, so the
 //     CRC-aided winner rule (scl.py:181-191) needs no stored decisions;
 //   * decisions are stored as 32-bit windows with an ancestor lane per window
-//     (a traceback); only the winner's path is reconstructed at the end.
+//     (a traceback in the caller's workspace); only the winner's path is
+//     reconstructed at the end.
 #pragma once
 #include "args.cuh"
 #include "scl_math.cuh"
