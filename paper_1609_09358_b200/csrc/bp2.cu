@@ -1,22 +1,25 @@
 // bp2.cu -- K1 v2: BP decoding with register-resident low stages and
-// warp-shuffle butterflies (sm_100a).  Same arithmetic and stop cadence as
-// k_bp_decode (bp.cu), which restates bp.py:120-217.
+// warp-shuffle butterflies (sm_100a).  Same stop cadence as k_bp_decode
+// (bp.cu), which restates bp.py:120-217; node update: bp_math.cuh::bp_pe2.
 //
 // Node ownership: thread t of the frame owns the Q = N / TPF consecutive nodes
 // base(t) .. base(t)+Q-1 with base(t) = warp*32Q + lane*Q.  Then
 //   * boundaries 1..B (B = log2 Q) join nodes inside one thread: register
 //     butterflies, no communication at all;
 //   * boundaries B+1..B+5 join nodes of lanes lane ^ 2^(j-1-B) of the same
-//     warp: each lane exchanges (R[j-1], L[j]) of its nodes with one shuffle
-//     pair and computes the node update of its own half of the element
-//     (i1 lanes:  g(a, l2 + r2) / g(l1, l2 + r2); i2 lanes: g(a, l1) + r2 /
-//     g(a, l1) + l2, clipped);
-//   * only boundaries above BW = B+5 go through shared memory, one CTA barrier
-//     each.
+//     warp: the lane pair splits the PEs (lo lane: nodes 0..Q/2-1, hi lane: the
+//     rest), exchanges the operands it lacks with shuffles and evaluates BOTH
+//     node updates of its PEs, so the shared operand's exponential is computed
+//     once per PE;
+//   * only boundaries above BW = B+5 go through shared memory, in radix-4
+//     pairs (the nodes b, b+h, b+2h, b+3h are closed under boundaries j and
+//     j+1): one CTA barrier per pair.
 // The message stages 1..BW-1 of a thread's nodes therefore live in registers
 // across iterations (the same thread owns the same nodes in both sweeps), and
-// shared memory holds only R[BW..n-1] and L[BW..n].  At N=1024, TPF=256 that is
-// 7 rows (28 KB) instead of 19, and 7 CTA barriers per iteration instead of 20.
+// shared memory holds only R[BW..n-1] and L[BW..n] (7 rows, 28 KB at N=1024,
+// TPF=256), the R sweep's kept exponentials 2^-|a| for the L sweep (N <= 2048),
+// and the decisions.  The frame's channel row arrives by a TMA bulk copy;
+// outputs are bit-packed with warp ballots.
 #include "args.cuh"
 #include "bp_math.cuh"
 
