@@ -43,7 +43,7 @@ extern "C" {
 #define PC_ERR_CUDA (-3)        /* a CUDA runtime call failed */
 #define PC_ERR_NO_DEVICE (-4)   /* no sm_100 device visible */
 
-#define PC_MAX_LOGN 12 /* N <= 4096 (N = 4096 BP: register/shuffle kernel, 1024 threads per frame) */
+#define PC_MAX_LOGN 12 /* N <= 4096 (N = 4096 BP: register/shuffle kernel, 512 threads per frame) */
 #define PC_MAX_LIST 32
 
 /* A polar code, described by device-resident tables built on the host from
@@ -66,8 +66,8 @@ typedef struct pc_code {
  * (4 MUFU, the pre-exponential-domain form; N = 1024/2048, parity studies); stop_mode 0 = crc,
  * 1 = reencode, 2 = none.  threads_per_frame 0 = library default.
  * kernel: 0 = auto (register/shuffle kernel when eligible), 1 = shared-memory
- * kernel, 2 = register/shuffle kernel (N = 128..4096, crc/none stop, no soft_x;
- * N = 4096 runs only on this kernel);
+ * kernel, 2 = register/shuffle kernel (N = 128..4096, crc/none stop; soft_x only
+ * at N = 4096, which runs only on this kernel);
  * a performance knob that does not change results. */
 typedef struct pc_bp_cfg {
     int32_t i_max, g_mode, stop_mode, threads_per_frame;

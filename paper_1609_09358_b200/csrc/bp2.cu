@@ -427,6 +427,21 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
             *reinterpret_cast<float2 *>(a.soft_u + (size_t)f * N + base + r) =
                 make_float2(su[r] * KOUT, su[r + 1] * KOUT);
     }
+    if constexpr (LOGN - 1 >= BW) {
+        // soft_x = L[n] + R[n] (bp.py:164-168); R[n] is not needed by the sweeps,
+        // so it is formed once here from the final R[n-1] row (shared memory).
+        if (a.soft_x != nullptr) {
+            __syncthreads();
+            const float *Rp = Rs + (LOGN - 1 - BW) * N;
+            for (int p = tid; p < N / 2; p += TPF) {
+                const int i1 = p, i2 = p + N / 2;
+                float o1, o2;
+                bp_pe2<GMODE, true>(Rp[i1], Lch[i2] + Rp[i2], Lch[i1], Rp[i2], lim, o1, o2);
+                a.soft_x[(size_t)f * N + i1] = (Lch[i1] + o1) * KOUT;
+                a.soft_x[(size_t)f * N + i2] = (Lch[i2] + o2) * KOUT;
+            }
+        }
+    }
     __syncthreads();
     // bit-pack with warp ballots: thread b of the pass owns bit b (coalesced
     // info_pos reads, one store per 32 bits)
@@ -505,7 +520,8 @@ bool bp2_eligible(const BpArgs &a, int tpf)
 {
     const int N = a.code.N;
     const int lo = N / 8 > 32 ? N / 8 : 32;
-    return a.code.n >= 7 && a.code.n <= 12 && a.stop_mode != 1 && a.soft_x == nullptr &&
+    // soft_x only where the smem kernel (bp.cu) has no room: N = 4096
+    return a.code.n >= 7 && a.code.n <= 12 && a.stop_mode != 1 && (a.soft_x == nullptr || a.code.n == 12) &&
            (tpf <= 0 || (tpf >= lo && tpf <= N / 2));
 }
 

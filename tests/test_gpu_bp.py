@@ -208,6 +208,20 @@ def test_minsum_bit_exact_vs_fp32_restatement(N, eb, count):
         assert np.array_equal(got.u_hat[f], u), f"frame {f}"
 
 
+def test_n4096_single_frame_api_soft_outputs():
+    """bp_decode at N=4096: soft_u and soft_x (L[n] + R[n], formed at exit by
+    the register/shuffle kernel) against the fp64 oracle."""
+    code = CodeConfig(4096, 2048, crc=16)
+    _, llr = make_frame(code, ebno_to_sigma(3.0, code.rate), frame_rng(4098, 0, 1))
+    llr = llr.astype(np.float32).astype(np.float64)
+    res = bp_decode(llr, code, BpConfig(stop_mode="crc"))
+    ref = oracle.bp_decode(llr, code, stop_mode="crc")
+    assert res.converged == ref["converged"] and res.iterations_used == ref["iterations_used"]
+    assert np.array_equal(res.u_hat, ref["u_hat"])
+    assert mixed_err(res.soft_u, ref["soft_u"]) <= 1e-3
+    assert mixed_err(res.soft_x, ref["soft_x"]) <= 1e-3
+
+
 def test_n4096_unsupported_paths_fail_loudly():
     """N=4096 state does not fit one SM for the shared-memory kernel: the
     re-encode stop and soft_x raise instead of silently falling back."""
