@@ -66,9 +66,10 @@ typedef struct pc_code {
  * (4 MUFU, the pre-exponential-domain form; N = 1024/2048, parity studies); stop_mode 0 = crc,
  * 1 = reencode, 2 = none.  threads_per_frame 0 = library default.
  * kernel: 0 = auto (register/shuffle kernel when eligible), 1 = shared-memory
- * kernel, 2 = register/shuffle kernel (N = 128..4096, crc/none stop; soft_x only
- * at N = 4096, which runs only on this kernel);
- * a performance knob that does not change results. */
+ * kernel, 2 = register/shuffle kernel (N = 128..4096, every stop rule, the
+ * re-encode stop with threads_per_frame >= 64; soft_x only at N = 4096, which
+ * runs only on this kernel); a performance knob: both kernels restate the same
+ * fp64 recursion in fp32 and may part only on certified near-ties. */
 typedef struct pc_bp_cfg {
     int32_t i_max, g_mode, stop_mode, threads_per_frame;
     float llr_max;

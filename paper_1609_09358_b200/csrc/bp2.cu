@@ -56,7 +56,7 @@ __host__ __device__ constexpr int bp2_keep_bytes(int logn, int tpf, int gmode)
     return bp2_keep(logn, tpf, gmode) * (1 << logn) * 2;
 }
 
-template <int LOGN, int TPF, int GMODE>
+template <int LOGN, int TPF, int GMODE, bool RE>
 __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
 {
     constexpr int N = 1 << LOGN;
@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
     float *Pa = Ls + NSL * N + N / 4; // kept exponentials, [(j - 2) * Q/2 + k][tid]
     __shared__ uint32_t frz[NW];
     __shared__ uint32_t red[NWARP];
+    __shared__ uint32_t xw[RE ? TPF : 1]; // re-encode stop: the warp-transformed bits of each thread
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int f = blockIdx.x;
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
             }
         }
         // ================= stop rule (crc or none) =================
-        if (a.stop_mode == 0) {
+        if (!RE && a.stop_mode == 0) {
             uint32_t syn = 0;
 #pragma unroll
             for (int r = 0; r < Q; ++r)
@@ -406,6 +407,50 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
             for (int w = 0; w < NWARP; ++w)
                 tot ^= red[w];
             stop = (tot == a.code.crc_offset);
+        }
+        if constexpr (RE && LOGN - 1 >= BW) {
+            {
+                // re-encode stop (bp.py:187): polar_transform(hard(soft_u)) == hard(L[n] + R[n]).
+                // R[n] comes from this iteration's R[n-1] row (the L sweep leaves it
+                // alone); x_hat lands as bytes in ub.  The transform of the thread's
+                // Q bits runs in registers (in-thread, then lane shuffles); the
+                // cross-warp stages read the other warps' words once: x_w = XOR of
+                // v_w' over the warps w' whose index contains w's bits.
+                const float *Rp = Rs + (LOGN - 1 - BW) * N;
+#pragma unroll 1
+                for (int p = tid; p < N / 2; p += TPF) {
+                    const int i1 = p, i2 = p + N / 2;
+                    float o1, o2;
+                    bp_pe2<GMODE, true>(Rp[i1], Lch[i2] + Rp[i2], Lch[i1], Rp[i2], lim, o1, o2);
+                    ub[i1] = (Lch[i1] + o1) < 0.0f;
+                    ub[i2] = (Lch[i2] + o2) < 0.0f;
+                }
+                uint32_t v = 0;
+#pragma unroll
+                for (int r = 0; r < Q; ++r)
+                    v |= (su[r] < 0.0f ? 1u : 0u) << r;
+#pragma unroll
+                for (int h = 1; h < Q; h <<= 1)
+                    v ^= (v >> h) & (h == 1 ? 0x55u : (h == 2 ? 0x33u : 0x0Fu));
+#pragma unroll
+                for (int s = 1; s < 32; s <<= 1) {
+                    const uint32_t pv = __shfl_xor_sync(0xffffffffu, v, s);
+                    if (!(lane & s))
+                        v ^= pv;
+                }
+                xw[tid] = v;
+                __syncthreads();
+                uint32_t x = 0;
+#pragma unroll
+                for (int w2 = 0; w2 < NWARP; ++w2)
+                    if ((w2 & warp) == warp)
+                        x ^= xw[w2 * 32 + lane];
+                uint32_t xh = 0;
+#pragma unroll
+                for (int r = 0; r < Q; ++r)
+                    xh |= (uint32_t)ub[base + r] << r;
+                stop = !__syncthreads_or(x != xh);
+            }
         }
         if (stop || it >= a.i_max)
             break;
@@ -467,6 +512,11 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
 #undef PAP
 #undef KEPT
 
+static int bp2_default_tpf(int N)
+{
+    return N >= 4096 ? 512 : (N / 4 >= 256 ? 256 : N / 4); // measured (tools/bp_tpf_probe.py)
+}
+
 static size_t bp2_smem_bytes(int logn, int tpf)
 {
     const int N = 1 << logn;
@@ -480,7 +530,12 @@ static size_t bp2_smem_bytes(int logn, int tpf)
 template <int LOGN, int TPF, int GMODE>
 static int launch_bp2_t(const BpArgs &a, cudaStream_t s)
 {
-    auto kern = k_bp2<LOGN, TPF, GMODE>;
+    // the re-encode stop is its own instantiation (its registers would cost the
+    // CRC kernel an occupancy step at N = 1024)
+    auto kern = k_bp2<LOGN, TPF, GMODE, false>;
+    if constexpr (GMODE != 2 && TPF >= 64)
+        if (a.stop_mode == 1)
+            kern = k_bp2<LOGN, TPF, GMODE, true>;
     const size_t smem = bp2_smem_bytes(LOGN, TPF) + bp2_keep_bytes(LOGN, TPF, GMODE);
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -496,7 +551,7 @@ static int launch_bp2_n(const BpArgs &a, int tpf, cudaStream_t s)
     constexpr int LO = N / 8 > 32 ? N / 8 : 32; // Q <= 8 nodes per thread (Q = 16 needs ~120+ registers)
     constexpr int HI = N / 2;                   // Q >= 2
     if (tpf <= 0)
-        tpf = N >= 4096 ? 512 : (N / 4 >= 256 ? 256 : N / 4); // measured (tools/bp_tpf_probe.py)
+        tpf = bp2_default_tpf(N);
     if (tpf < LO || tpf > HI)
         return PC_ERR_UNSUPPORTED;
 #define PC_BP2_CASE(T)                                                                                                 \
@@ -513,22 +568,31 @@ static int launch_bp2_n(const BpArgs &a, int tpf, cudaStream_t s)
 #undef PC_BP2_CASE
 }
 
-// K1 v2 covers N = 128 .. 4096 with the crc / none stop rules and no soft_x.
-// N = 4096 runs one 512-thread CTA per frame (Q = 8): 9 shared rows (144 KB) plus
-// 80 KB of kept exponentials, one CTA per SM.
+// K1 v2 covers N = 128 .. 4096 with every stop rule (re-encode: TPF >= 64) and
+// soft_x at N = 4096 (below, the shared-memory kernel in bp.cu forms it).
+// N = 4096 runs one 512-thread CTA per frame (Q = 8): 9 shared rows (144 KB),
+// no kept exponentials, one CTA per SM.
 bool bp2_eligible(const BpArgs &a, int tpf)
 {
     const int N = a.code.N;
     const int lo = N / 8 > 32 ? N / 8 : 32;
     // soft_x only where the smem kernel (bp.cu) has no room: N = 4096
-    return a.code.n >= 7 && a.code.n <= 12 && a.stop_mode != 1 && (a.soft_x == nullptr || a.code.n == 12) &&
-           (tpf <= 0 || (tpf >= lo && tpf <= N / 2));
+    if (!(a.code.n >= 7 && a.code.n <= 12 && (a.soft_x == nullptr || a.code.n == 12) &&
+          (tpf <= 0 || (tpf >= lo && tpf <= N / 2))))
+        return false;
+    if (a.stop_mode != 1)
+        return true;
+    // the re-encode stop needs R[n-1] in shared memory: log2 TPF >= 6
+    const int t = tpf > 0 ? tpf : bp2_default_tpf(N);
+    return t >= 64;
 }
 
 int launch_bp2(const BpArgs &a, int g_mode, int tpf, cudaStream_t s)
 {
     if (a.B == 0)
         return PC_OK;
+    if (!bp2_eligible(a, tpf) || (g_mode == 2 && a.stop_mode == 1))
+        return PC_ERR_UNSUPPORTED;
     const int n = a.code.n;
     if (g_mode == 2) { // exact g, per-g form (parity studies)
         switch (n) {

@@ -87,17 +87,17 @@ def near_tie(llr, code, k, got_u_k, g_mode="exact"):
     return bool(diff.size) and worst < NEAR_TIE_SOFT, worst
 
 
-def ill_conditioned(llr, code, ref_it, ref_cv, trials=6, eps=1e-6):
+def ill_conditioned(llr, code, ref_it, ref_cv, trials=6, eps=1e-6, stop_mode="crc"):
     """The fp64 reference itself changes its (converged, iterations) under a
     relative input perturbation of eps (far below fp32 resolution of the
     messages): the frame's decision trajectory is ill-conditioned."""
     rng = np.random.default_rng(int(abs(llr[:8]).sum() * 1e6) % (2**32))
     pert = llr * (1.0 + eps * rng.choice([-1.0, 1.0], size=(trials, llr.size)))
-    _, it, cv = oracle.bp_batch(pert, code, stop_mode="crc")
+    _, it, cv = oracle.bp_batch(pert, code, stop_mode=stop_mode)
     return bool(np.any(it != ref_it) or np.any(cv.astype(bool) != bool(ref_cv)))
 
 
-def _check_decisions(name, ref_u, ref_it, ref_cv, got, llrs=None, code=None):
+def _check_decisions(name, ref_u, ref_it, ref_cv, got, llrs=None, code=None, stop_mode="crc"):
     """Flags and iteration counts must agree; u_hat must agree where both converged.
 
     A non-converged frame's u_hat is the chaotic state after i_max iterations
@@ -122,7 +122,7 @@ def _check_decisions(name, ref_u, ref_it, ref_cv, got, llrs=None, code=None):
                 k = min(int(ref_it[f]), int(got.iterations_used[f]))
                 dev_k = bp_decode_batch(llrs[f:f + 1], code, BpConfig(i_max=k, stop_mode="none"))
                 ok, worst = near_tie(llrs[f], code, k, dev_k.u_hat[0])
-                if ok or ill_conditioned(llrs[f], code, int(ref_it[f]), ref_cv[f]):
+                if ok or ill_conditioned(llrs[f], code, int(ref_it[f]), ref_cv[f], stop_mode=stop_mode):
                     certified.append(rec + (worst,))
                     continue
             bad_early.append(rec)
@@ -222,13 +222,36 @@ def test_n4096_single_frame_api_soft_outputs():
     assert mixed_err(res.soft_x, ref["soft_x"]) <= 1e-3
 
 
-def test_n4096_unsupported_paths_fail_loudly():
-    """N=4096 state does not fit one SM for the shared-memory kernel: the
-    re-encode stop and soft_x raise instead of silently falling back."""
-    code = CodeConfig(4096, 2048, crc=16)
-    llrs = np.zeros((2, 4096))
-    with pytest.raises(RuntimeError):
-        bp_decode_batch(llrs, code, BpConfig(stop_mode="reencode"))
+@pytest.mark.parametrize("N,eb,count", [(1024, 2.0, 400), (2048, 2.5, 200), (4096, 2.5, 96)])
+def test_reencode_stop_vs_oracle(N, eb, count):
+    """The re-encode stop (the reference's default, bp.py:187) in the
+    register/shuffle kernel: R[n] from the iteration's R[n-1] row, the
+    transform of hard(soft_u) in registers, against the fp64 oracle."""
+    code = CodeConfig(N, N // 2, crc=16)
+    sigma = ebno_to_sigma(eb, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(77, N, f))[1] for f in range(count)])
+    llrs = llrs.astype(np.float32).astype(np.float64)
+    ref_u, ref_it, ref_cv = oracle.bp_batch(llrs, code, stop_mode="reencode")
+    got = bp_decode_batch(llrs, code, BpConfig(i_max=50, stop_mode="reencode"))
+    assert got.converged.mean() > 0.5
+    late = _check_decisions(f"reencode{N}", ref_u, ref_it, ref_cv, got, llrs, code, stop_mode="reencode")
+    print("near-tie frames:", late)
+
+
+def test_reencode_kernels_agree(monkeypatch):
+    """The shared-memory kernel (bp.cu, PC_BP_KERNEL=1) and the register/shuffle
+    kernel (PC_BP_KERNEL=2) stop on the same iteration for the re-encode rule."""
+    code = CodeConfig(1024, 512, crc=None)
+    sigma = ebno_to_sigma(2.5, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(78, 0, f))[1] for f in range(256)])
+    monkeypatch.setenv("PC_BP_KERNEL", "1")
+    a = bp_decode_batch(llrs, code, BpConfig(stop_mode="reencode"))
+    monkeypatch.setenv("PC_BP_KERNEL", "2")
+    b = bp_decode_batch(llrs, code, BpConfig(stop_mode="reencode"))
+    same = (a.iterations_used == b.iterations_used) & (a.converged == b.converged)
+    assert same.mean() >= 0.98
+    both = a.converged & b.converged & same
+    assert all(np.array_equal(a.u_hat[f], b.u_hat[f]) for f in np.flatnonzero(both))
 
 
 def test_single_frame_api_and_soft_outputs():
