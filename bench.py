@@ -9,11 +9,13 @@ EVERY sweep point.  value = decoded payload Gbit/s over the whole sweep
 frame latency, gamma and FER are in "sweep".
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py --workload c1     # BASELINE configs[0]: BP N=128, 2 dB
+    python bench.py --workload c2     # BASELINE configs[1]: SCL N=1024 L=32, 1-4 dB
     python bench.py --workload c4     # BASELINE configs[3]: large-batch BP N=4096, 2 and 3 dB
     python bench.py --workload c5     # BASELINE configs[4]: SCL N=2048 list-size sweep L=1..32
 
-The default workload (c3) is the headline; c4 and c5 print their own JSON line
-(same contract keys) for the other BASELINE configurations.
+The default workload (c3) is the headline; the others print their own JSON
+line (same contract keys) for the other BASELINE configurations.
 
 Multi-GPU: frames shard by index (weak scaling, no collective on the data
 path); timing is the max over ranks of the barrier-bracketed device time.
@@ -376,6 +378,16 @@ def _gpu_common(args):
     return torch, dist, rank, world, local
 
 
+def _cpu_sample(sample, fpp, fixed, min_s=2.0, cap=1 << 16):
+    """Run sample(fpp) -> (busy_s, bits), growing fpp 4x until the oracle's
+    decode takes at least min_s of wall (a bounded but measurable sample)."""
+    busy, bits = sample(fpp)
+    while not fixed and busy < min_s and fpp < cap:
+        fpp = min(cap, fpp * 4)
+        busy, bits = sample(fpp)
+    return fpp, busy, bits
+
+
 def _xu_peak_gg(torch, dev, mpg):
     peak_mhz = 1965.0
     try:
@@ -386,11 +398,25 @@ def _xu_peak_gg(torch, dev, mpg):
     return sms * 16 * peak_mhz * 1e6 / mpg / 1e9
 
 
-def run_c4(args):
-    """BASELINE configs[3]: inter-frame BP N=4096 K=2048 (2032 payload + CRC-16),
-    i_max=50, CRC stop, Eb/N0 2 and 3 dB; frames sharded across ranks (weak)."""
+BP_WORKLOADS = {
+    "c1": {"N": 128, "K": 64, "pts": (2.0,), "pid": 30, "B": 1 << 20, "cfg": 0, "fixed_cap": True,
+           "metric": "decoded info Gbit/s, inter-frame BP N=128 R=1/2 (i_max=50, CRC stop), Eb/N0 2 dB",
+           "workload": "BP-only N=128 K=64 (48 payload + CRC-16) i_max=50 CRC stop (BASELINE configs[0])",
+           "kernel": "k_bp2<7,32,0> (register/shuffle BP, one warp per frame, kept exponentials)"},
+    "c4": {"N": 4096, "K": 2048, "pts": (2.0, 3.0), "pid": 10, "B": 1 << 16, "cfg": 3,
+           "metric": "decoded info Gbit/s, inter-frame BP N=4096 R=1/2 (i_max=50, CRC stop), Eb/N0 2 and 3 dB",
+           "workload": "BP-only N=4096 K=2048 (2032 payload + CRC-16) i_max=50 CRC stop (BASELINE configs[3])",
+           "kernel": "k_bp2<12,512,0> (register/shuffle BP, 512 threads/frame)"},
+}
+
+
+def run_bp_workload(args):
+    """BASELINE configs[0] (c1: BP N=128 K=64, 2 dB) and configs[3] (c4:
+    inter-frame BP N=4096 K=2048, 2 and 3 dB): i_max=50, CRC stop; frames
+    sharded across ranks (weak)."""
     import ctypes
 
+    wl = BP_WORKLOADS[args.workload]
     torch, dist, rank, world, local = _gpu_common(args)
     from paper_1609_09358_b200 import BpConfig, CodeConfig
     from paper_1609_09358_b200 import _native as nat
@@ -398,17 +424,17 @@ def run_c4(args):
     from paper_1609_09358_b200.shard import max_over_ranks, shard_range
 
     lib = nat.load()
-    n4, k4, pts = 4096, 2048, (2.0, 3.0)
+    n4, k4, pts = wl["N"], wl["K"], wl["pts"]
     code = CodeConfig(n4, k4, crc=16)
     m, MW = code.message_len, (code.message_len + 31) // 32
-    B = args.frames if args.frames != (1 << 17) else (1 << 16)
+    B = args.frames if args.frames != (1 << 17) else wl["B"]
     dev = torch.device("cuda", local)
     dc = nat.device_code(code)
     st = nat.stream_handle()
     llr = torch.empty((len(pts), B, n4), dtype=torch.float32, device=dev)
     msg = torch.empty((len(pts), B, MW), dtype=torch.int32, device=dev)
     for p, eb in enumerate(pts):
-        nat.check(lib.pc_gen_frames(SEED, 10 + p, shard_range(rank, world, B)[0], B, ebno_to_sigma(eb, code.rate),
+        nat.check(lib.pc_gen_frames(SEED, wl["pid"] + p, shard_range(rank, world, B)[0], B, ebno_to_sigma(eb, code.rate),
                                     dc.ref, msg[p].data_ptr(), llr[p].data_ptr(), st), "pc_gen_frames")
     pay = torch.empty((B, MW), dtype=torch.int32, device=dev)
     iters = torch.empty((len(pts), B), dtype=torch.int32, device=dev)
@@ -457,7 +483,8 @@ def run_c4(args):
     value = world * B * m * len(pts) * args.steps / (max_ms * 1e-3) / 1e9
     g_step = int(it_sum.sum()) * 2 * code.n * n4
     achieved = g_step / (sum(pt_ms) * 1e-3) / 1e9
-    peak = _xu_peak_gg(torch, dev, mufu_per_alg_g(code.n, False))  # N = 4096: no kept exponentials, FMA exp2 in both sweeps
+    # N <= 2048 keeps the R sweep's exponentials; N = 4096 does not (FMA exp2 in both sweeps)
+    peak = _xu_peak_gg(torch, dev, mufu_per_alg_g(code.n, code.n <= 11))
     # e2e: pinned host LLRs -> device, decode, payload + flags -> host, every step
     host = [torch.empty((B, n4), dtype=torch.float32, pin_memory=True) for _ in pts]
     for p in range(len(pts)):
@@ -497,6 +524,31 @@ def run_c4(args):
             conv_h[p].copy_(conv[p], non_blocking=True)
         torch.cuda.synchronize()
 
+    fixed = None
+    if wl.get("fixed_cap"):
+        # BASELINE configs[0]'s fixed iteration cap: stop rule "none", every frame
+        # runs exactly i_max iterations (deterministic work for the roofline)
+        cfg_none = BpConfig(i_max=IMAX, stop_mode="none").native()
+
+        def step_none():
+            nat.check(lib.pc_bp_decode(llr[0].data_ptr(), B, dc.ref, ctypes.byref(cfg_none), None, pay.data_ptr(),
+                                       None, None, iters[0].data_ptr(), conv[0].data_ptr(), None, st), "bp none")
+
+        for _ in range(args.warmup):
+            step_none()
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            step_none()
+        b.record()
+        barrier()
+        fms = max_over_ranks(a.elapsed_time(b) / args.steps, device=COMM)
+        fg = B * IMAX * 2 * code.n * n4 / (fms * 1e-3) / 1e9
+        fixed = {"stop_mode": "none", "i_max": IMAX, "ms_per_batch": fms,
+                 "frame_iterations_per_s": world * B * IMAX / (fms * 1e-3),
+                 "gbps": world * B * m / (fms * 1e-3) / 1e9, "achieved_gg_s": fg, "frac": fg / peak}
     e2e_run(1)
     barrier()
     te = time.perf_counter()
@@ -510,34 +562,39 @@ def run_c4(args):
             from paper_1609_09358_b200.channel import frame_rng, make_frame
 
             threads = oracle.cpu_count()
-            fpp = args.cpu_frames or max(32, 2 * threads)
-            busy, bits = 0.0, 0
-            for p, eb in enumerate(pts):
-                sig = ebno_to_sigma(eb, code.rate)
-                L = np.array([make_frame(code, sig, frame_rng(SEED, 10 + p, f))[1] for f in range(fpp)])
-                t = time.perf_counter()
-                oracle.bp_batch(L, code, i_max=IMAX, stop_mode="crc", nthreads=threads)
-                busy += time.perf_counter() - t
-                bits += fpp * m
+
+            def sample(fpp):
+                busy, bits = 0.0, 0
+                for p, eb in enumerate(pts):
+                    sig = ebno_to_sigma(eb, code.rate)
+                    L = np.array([make_frame(code, sig, frame_rng(SEED, wl["pid"] + p, f))[1] for f in range(fpp)])
+                    t = time.perf_counter()
+                    oracle.bp_batch(L, code, i_max=IMAX, stop_mode="crc", nthreads=threads)
+                    busy += time.perf_counter() - t
+                    bits += fpp * m
+                return busy, bits
+
+            fpp, busy, bits = _cpu_sample(sample, args.cpu_frames or max(32, 2 * threads), bool(args.cpu_frames))
             cpu = {"value": bits / busy / 1e9, "unit": "Gbit/s", "cores": threads, "kind": "port",
                    "sample": f"{fpp} frames per Eb/N0 point x {len(pts)} points, {busy:.1f} s of CPU wall "
                              f"(fp64 oracle port of bp_decode, all host threads)"}
         line = {
-            "metric": "decoded info Gbit/s, inter-frame BP N=4096 R=1/2 (i_max=50, CRC stop), Eb/N0 2 and 3 dB",
+            "metric": wl["metric"],
             "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (device Philox-keyed BPSK/AWGN frames, resident in HBM before timing)",
-            "config": {"workload": "BP-only N=4096 K=2048 (2032 payload + CRC-16) i_max=50 CRC stop (BASELINE "
-                                   "configs[3])", "frames_per_point_per_gpu": B, "ebno_db": list(pts),
+            "config": {"workload": wl["workload"], "frames_per_point_per_gpu": B, "ebno_db": list(pts),
                        "parallelism": f"frame-sharded x{world}",
                        "l2": f"inputs larger than L2 ({B * n4 * 4 / 1e6:.0f} MB per point)"},
             "sweep": [{"ebno_db": eb, "gbps": world * B * m / (pt_ms[p] * 1e-3) / 1e9, "ms": pt_ms[p],
                        "mean_bp_iters": float(it_sum[p]) / B, "fer": float(errs_h[p, 1]) / B,
                        "ber": float(errs_h[p, 0]) / (B * m)} for p, eb in enumerate(pts)],
             "roofline": {"bound": "xu", "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": "k_bp2<12,512,0> (register/shuffle BP, 512 threads/frame)",
+                         "traffic": None, "kernel": wl["kernel"],
                          "note": "exact-g node updates/s (2nN per frame-iteration) vs 148 SM x 16 MUFU/clk / "
-                                 "MUFU per algorithmic g (7 per PE, R[n] not computed)"},
+                                 f"{mufu_per_alg_g(code.n, code.n <= 11):.3f} MUFU per algorithmic g "
+                                 "(bench.mufu_per_alg_g; R[n] not computed)"},
+            "fixed_cap": fixed,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "Gbit/s", "h2d_bytes_per_step": B * n4 * 4 * len(pts),
                     "d2h_bytes_per_step": B * (MW * 4 + 1) * len(pts)},
@@ -550,13 +607,27 @@ def run_c4(args):
     return 0
 
 
-def run_c5(args):
-    """BASELINE configs[4]: SCL N=2048 K=1024 (1008 payload + CRC-16) at 2 dB,
-    L = 1, 2, 4, 8, 16, 32: batch throughput (frames/s, Gbit/s), the batch p50
-    frame latency (reference semantic: batch start -> frame decision) and the
-    single-frame latency (one frame alone on the GPU)."""
+SCL_WORKLOADS = {
+    "c2": {"N": 1024, "K": 512, "rows": [(32, eb, 40 + p) for p, eb in enumerate(EBNO)], "B": 16384,
+           "metric": "SCL decoded info Gbit/s, N=1024 R=1/2 L=32, Eb/N0 1-4 dB (sweep aggregate)",
+           "workload": "CRC-aided SCL N=1024 K=512 (496 payload + CRC-16) L=32, Eb/N0 1-4 dB step 0.5 "
+                       "(BASELINE configs[1]); value = sum of bits / sum of time over the points"},
+    "c5": {"N": 2048, "K": 1024, "rows": [(L, 2.0, 20) for L in (1, 2, 4, 8, 16, 32)], "B": 10_000,
+           "metric": "SCL decoded info Gbit/s and latency vs list size, N=2048 R=1/2, Eb/N0 2 dB",
+           "workload": "CRC-aided SCL N=2048 K=1024 (1008 payload + CRC-16) L=1..32 at 2 dB (BASELINE "
+                       "configs[4]); value = the L=32 line"},
+}
+
+
+def run_scl_workload(args):
+    """BASELINE configs[1] (c2: SCL N=1024 K=512 L=32 over 1-4 dB) and
+    configs[4] (c5: SCL N=2048 K=1024 at 2 dB, L = 1, 2, 4, 8, 16, 32): batch
+    throughput (frames/s, Gbit/s), the batch p50 frame latency (reference
+    semantic: batch start -> frame decision) and the single-frame latency (one
+    frame alone on the GPU) per row."""
     import ctypes
 
+    wl = SCL_WORKLOADS[args.workload]
     torch, dist, rank, world, local = _gpu_common(args)
     from paper_1609_09358_b200 import CodeConfig, SclConfig
     from paper_1609_09358_b200 import _native as nat
@@ -564,21 +635,19 @@ def run_c5(args):
     from paper_1609_09358_b200.shard import max_over_ranks, shard_range
 
     lib = nat.load()
-    n5, k5, eb = 2048, 1024, 2.0
+    n5, k5 = wl["N"], wl["K"]
     code = CodeConfig(n5, k5, crc=16)
     m, MW = code.message_len, (code.message_len + 31) // 32
-    B = args.frames if args.frames != (1 << 17) else 10_000
+    B = args.frames if args.frames != (1 << 17) else wl["B"]
     dev = torch.device("cuda", local)
     dc = nat.device_code(code)
     st = nat.stream_handle()
     llr = torch.empty((B, n5), dtype=torch.float32, device=dev)
     msg = torch.empty((B, MW), dtype=torch.int32, device=dev)
-    nat.check(lib.pc_gen_frames(SEED, 20, shard_range(rank, world, B)[0], B, ebno_to_sigma(eb, code.rate), dc.ref,
-                                msg.data_ptr(), llr.data_ptr(), st), "pc_gen_frames")
     pay = torch.empty((B, MW), dtype=torch.int32, device=dev)
     tdone = torch.empty(B, dtype=torch.int64, device=dev)
     t0s = torch.empty(1, dtype=torch.int64, device=dev)
-    errs = torch.zeros((6, 2), dtype=torch.int64, device=dev)
+    errs = torch.zeros((len(wl["rows"]), 2), dtype=torch.int64, device=dev)
     rows = []
 
     def barrier():
@@ -586,9 +655,11 @@ def run_c5(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    total_ms = 0.0
+    total_ms, total_bits = 0.0, 0
     with ClockSampler(local) as clocks:
-        for li, L in enumerate((1, 2, 4, 8, 16, 32)):
+        for li, (L, eb, pid) in enumerate(wl["rows"]):
+            nat.check(lib.pc_gen_frames(SEED, pid, shard_range(rank, world, B)[0], B, ebno_to_sigma(eb, code.rate),
+                                        dc.ref, msg.data_ptr(), llr.data_ptr(), st), "pc_gen_frames")
             cfg = SclConfig(L).native()
 
             def dec(nf, stamp=False):
@@ -610,6 +681,7 @@ def run_c5(args):
             barrier()
             ms = max_over_ranks(a.elapsed_time(b) / args.steps, device=COMM)
             total_ms += ms
+            total_bits += world * B * m
             dec(B, stamp=True)
             nat.check(lib.pc_count_errors(pay.data_ptr(), msg.data_ptr(), B, m, errs[li].data_ptr(), st), "count")
             torch.cuda.synchronize()
@@ -625,7 +697,7 @@ def run_c5(args):
                 torch.cuda.synchronize()
                 one.append(a1.elapsed_time(b1))
             e = errs[li].cpu().numpy()
-            rows.append({"L": L, "ms_per_batch": ms, "frames_per_s": world * B / (ms * 1e-3),
+            rows.append({"L": L, "ebno_db": eb, "ms_per_batch": ms, "frames_per_s": world * B / (ms * 1e-3),
                          "gbps": world * B * m / (ms * 1e-3) / 1e9, "batch_p50_latency_ms": p50,
                          "single_frame_latency_ms": float(np.median(one[5:])), "fer": float(e[1]) / B,
                          "ber": float(e[0]) / (B * m)})
@@ -636,28 +708,31 @@ def run_c5(args):
             from paper_1609_09358_b200.channel import frame_rng, make_frame
 
             threads = oracle.cpu_count()
-            fpp = args.cpu_frames or max(64, 4 * threads)
+            L, eb, pid = wl["rows"][-1]
             sig = ebno_to_sigma(eb, code.rate)
-            Lr = np.array([make_frame(code, sig, frame_rng(SEED, 20, f))[1] for f in range(fpp)])
-            t = time.perf_counter()
-            oracle.scl_batch(Lr, code, 32, nthreads=threads)
-            busy = time.perf_counter() - t
+
+            def sample(fpp):
+                Lr = np.array([make_frame(code, sig, frame_rng(SEED, pid, f))[1] for f in range(fpp)])
+                t = time.perf_counter()
+                oracle.scl_batch(Lr, code, L, nthreads=threads)
+                return time.perf_counter() - t, fpp * m
+
+            fpp, busy, _ = _cpu_sample(sample, args.cpu_frames or max(64, 4 * threads), bool(args.cpu_frames))
             cpu = {"value": fpp * m / busy / 1e9, "unit": "Gbit/s", "cores": threads, "kind": "port",
-                   "sample": f"{fpp} frames at L=32, {busy:.1f} s of CPU wall (fp64 oracle port of scl_decode)"}
-        l32 = rows[-1]
+                   "sample": f"{fpp} frames at L={L}, {eb} dB, {busy:.1f} s of CPU wall "
+                             "(fp64 oracle port of scl_decode)"}
+        value = rows[-1]["gbps"] if args.workload == "c5" else total_bits / (total_ms * 1e-3) / 1e9
         line = {
-            "metric": "SCL decoded info Gbit/s and latency vs list size, N=2048 R=1/2, Eb/N0 2 dB",
-            "value": l32["gbps"], "unit": "Gbit/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "metric": wl["metric"],
+            "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (device Philox-keyed BPSK/AWGN frames, resident in HBM before timing)",
-            "config": {"workload": "CRC-aided SCL N=2048 K=1024 (1008 payload + CRC-16) L=1..32 at 2 dB (BASELINE "
-                                   "configs[4]); value = the L=32 line", "frames_per_gpu": B,
-                       "parallelism": f"frame-sharded x{world}",
+            "config": {"workload": wl["workload"], "frames_per_gpu": B, "parallelism": f"frame-sharded x{world}",
                        "l2": f"inputs {B * n5 * 4 / 1e6:.0f} MB, decode time per batch >> L2 refill"},
-            "list_sweep": rows,
+            "list_sweep" if args.workload == "c5" else "sweep": rows,
             "roofline": None,
             "cpu_baseline": cpu,
-            "gpu_launches": args.steps * 6,
+            "gpu_launches": args.steps * len(rows),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -676,15 +751,16 @@ def main():
     ap.add_argument("--chunk", type=int, default=0, help="frames per BP/SCL chunk (0 = whole batch)")
     ap.add_argument("--cpu-frames", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "c5"],
-                    help="c3 = hybrid sweep (headline); c4 = BP N=4096; c5 = SCL N=2048 list-size sweep")
+    ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="c3 = hybrid sweep (headline); c1 = BP N=128; c2 = SCL N=1024 L=32 sweep; "
+                         "c4 = BP N=4096; c5 = SCL N=2048 list-size sweep")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
-    if args.workload == "c4":
-        return run_c4(args)
-    if args.workload == "c5":
-        return run_c5(args)
+    if args.workload in BP_WORKLOADS:
+        return run_bp_workload(args)
+    if args.workload in SCL_WORKLOADS:
+        return run_scl_workload(args)
     return run_gpu(args)
 
 

@@ -175,8 +175,17 @@ __device__ __noinline__ float frozen_prefix(const float *ch, float *llr, uint32_
 
 } // namespace s3
 
+#ifndef PC_SCL3_MAXREG
+#define PC_SCL3_MAXREG 0
+#endif
+#if PC_SCL3_MAXREG > 0
+#define PC_SCL3_BOUNDS __maxnreg__(PC_SCL3_MAXREG)
+#else
+#define PC_SCL3_BOUNDS __launch_bounds__(128)
+#endif
+
 template <int L, bool FEX, int NV>
-__global__ void __launch_bounds__(128) k_scl3(const SclArgs a)
+__global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
 {
     using namespace s3;
     constexpr int F = 32 / L;

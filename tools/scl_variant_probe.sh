@@ -4,7 +4,7 @@
 for lib in "$@"; do
   cp "$lib" paper_1609_09358_b200/libpolarcuda.so
   echo "== $lib"
-  timeout 100 python tools/scl_ab.py 1024 512 32 1.5 8192 > /tmp/ab.log 2>&1; grep -E "v3 nv=-1" /tmp/ab.log; grep -c "True, True, True, True" /tmp/ab.log
-  timeout 100 python tools/scl_ab.py 2048 1024 32 2.0 4096 > /tmp/ab.log 2>&1; grep -E "v3 nv=-1" /tmp/ab.log; grep -c "True, True, True, True" /tmp/ab.log
-  timeout 100 python tools/scl_ab.py 2048 1024 8 2.0 4096 > /tmp/ab.log 2>&1; grep -E "v3 nv=-1" /tmp/ab.log; grep -c "True, True, True, True" /tmp/ab.log
+  timeout 100 python tools/scl_ab.py 1024 512 32 1.5 8192 > /tmp/ab.log 2>&1; grep -E "v3" /tmp/ab.log; grep -c "True, True, True, True" /tmp/ab.log
+  timeout 100 python tools/scl_ab.py 2048 1024 32 2.0 4096 > /tmp/ab.log 2>&1; grep -E "v3" /tmp/ab.log; grep -c "True, True, True, True" /tmp/ab.log
+  timeout 100 python tools/scl_ab.py 2048 1024 8 2.0 4096 > /tmp/ab.log 2>&1; grep -E "v3" /tmp/ab.log; grep -c "True, True, True, True" /tmp/ab.log
 done
