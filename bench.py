@@ -402,7 +402,7 @@ BP_WORKLOADS = {
     "c1": {"N": 128, "K": 64, "pts": (2.0,), "pid": 30, "B": 1 << 20, "cfg": 0, "fixed_cap": True,
            "metric": "decoded info Gbit/s, inter-frame BP N=128 R=1/2 (i_max=50, CRC stop), Eb/N0 2 dB",
            "workload": "BP-only N=128 K=64 (48 payload + CRC-16) i_max=50 CRC stop (BASELINE configs[0])",
-           "kernel": "k_bp2<7,32,0> (register/shuffle BP, one warp per frame, kept exponentials)"},
+           "kernel": "k_bp2<7,32,0,persistent> (register/shuffle BP, one warp per frame, kept exponentials)"},
     "c4": {"N": 4096, "K": 2048, "pts": (2.0, 3.0), "pid": 10, "B": 1 << 16, "cfg": 3,
            "metric": "decoded info Gbit/s, inter-frame BP N=4096 R=1/2 (i_max=50, CRC stop), Eb/N0 2 and 3 dB",
            "workload": "BP-only N=4096 K=2048 (2032 payload + CRC-16) i_max=50 CRC stop (BASELINE configs[3])",
@@ -441,6 +441,8 @@ def run_bp_workload(args):
     conv = torch.empty((len(pts), B), dtype=torch.uint8, device=dev)
     errs = torch.zeros((len(pts), 2), dtype=torch.int64, device=dev)
     cfg = BpConfig(i_max=IMAX, stop_mode="crc").native()
+    work = torch.empty(1, dtype=torch.int32, device=dev)  # frame counter: persistent K1 at small N
+    cfg.work = work.data_ptr()
 
     def step(events=None):
         for p in range(len(pts)):
@@ -529,6 +531,7 @@ def run_bp_workload(args):
         # BASELINE configs[0]'s fixed iteration cap: stop rule "none", every frame
         # runs exactly i_max iterations (deterministic work for the roofline)
         cfg_none = BpConfig(i_max=IMAX, stop_mode="none").native()
+        cfg_none.work = work.data_ptr()
 
         def step_none():
             nat.check(lib.pc_bp_decode(llr[0].data_ptr(), B, dc.ref, ctypes.byref(cfg_none), None, pay.data_ptr(),

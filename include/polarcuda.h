@@ -74,6 +74,12 @@ typedef struct pc_bp_cfg {
     int32_t i_max, g_mode, stop_mode, threads_per_frame;
     float llr_max;
     int32_t kernel;
+    /* Optional 4 bytes of device scratch, private to this call's stream: the
+     * frame counter of the persistent register/shuffle kernel (one CTA per
+     * resident slot, frames taken from the counter; 14% faster at N = 128,
+     * where frames of 1..i_max iterations otherwise leave CTA slots empty).
+     * NULL = one CTA per frame.  Does not change results. */
+    int32_t *work;
 } pc_bp_cfg_t;
 
 /* SclConfig, scl.py:39-66.  L in {1,2,4,8,16,32}.  virtual_levels: how many of

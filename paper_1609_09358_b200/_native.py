@@ -62,6 +62,7 @@ class PcBpCfg(C.Structure):
         ("threads_per_frame", C.c_int32),
         ("llr_max", C.c_float),
         ("kernel", C.c_int32),
+        ("work", C.c_void_p),
     ]
 
 
@@ -204,8 +205,25 @@ class DeviceCode:
     def ref(self):
         return C.byref(self.struct)
 
+    def scl_workspace_bytes(self, ncfg) -> int:
+        nbytes = int(load().pc_scl_workspace_bytes(self.ref, C.byref(ncfg)))
+        if nbytes < 0:
+            raise RuntimeError("pc_scl_workspace_bytes rejected the configuration")
+        return nbytes
+
+    def new_scl_workspace(self, ncfg, stream=None):
+        """A workspace private to one caller (torch caching allocator; recorded
+        on ``stream`` so it is not reused before that stream's launch ends)."""
+        import torch
+
+        ws = torch.empty((self.scl_workspace_bytes(ncfg) + 3) // 4, dtype=torch.int32, device=self.device)
+        if stream is not None:
+            ws.record_stream(stream)
+        return ws
+
     def scl_workspace(self, ncfg):
-        """Device workspace for pc_scl_decode with this code and PcSclCfg (cached by size)."""
+        """Device workspace for pc_scl_decode with this code and PcSclCfg (cached
+        by size and shared: for callers that order their launches on one stream)."""
         import torch
 
         nbytes = int(load().pc_scl_workspace_bytes(self.ref, C.byref(ncfg)))

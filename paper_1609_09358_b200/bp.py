@@ -238,6 +238,10 @@ def bp_decode_batch(
     pw = torch.empty((B, MW), dtype=torch.int32, device=dev) if payload else None
     dc = nat.device_code(code)
     ncfg = cfg.native()
+    wk = torch.empty(1, dtype=torch.int32, device=dev)  # frame counter of the persistent kernel (small N)
+    if stream is not None:
+        wk.record_stream(stream)  # freed to the caching allocator only after the launch on `stream`
+    ncfg.work = wk.data_ptr()
     nat.check(
         lib.pc_bp_decode(
             nat.ptr(x), B, dc.ref, C_byref(ncfg), nat.ptr(u), nat.ptr(pw), nat.ptr(su), nat.ptr(sx),

@@ -15,6 +15,7 @@ struct BpArgs {
     int32_t *iters;
     uint8_t *conv;
     uint64_t *t_done;
+    int32_t *work; // frame counter of the persistent K1 variant (nullptr: one CTA per frame)
 };
 
 struct SclArgs {

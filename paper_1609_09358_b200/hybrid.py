@@ -175,8 +175,11 @@ class HybridDecoder:
         self.counts = torch.zeros(self.nchunks_max, dtype=torch.int32, **z)
         # stamps per chunk: [start, bp_end, scl_start, scl_end]
         self.stamps = torch.zeros((self.nchunks_max, 4), dtype=torch.int64, **z)
-        # one K3 workspace for all chunks: their SCL launches are ordered on one stream
-        self.scl_ws = self.dc_scl.scl_workspace(self.nscl)
+        # this decoder's own K3 workspace (all its chunks' SCL launches are ordered
+        # on one stream) and K1 frame counter (persistent K1 at small N)
+        self.scl_ws = self.dc_scl.new_scl_workspace(self.nscl)
+        self.bp_work = torch.empty(1, dtype=torch.int32, **z)
+        self.nbp.work = self.bp_work.data_ptr()
         self.s_bp = torch.cuda.Stream(device=dev)
         # The list decoder's persistent warps get the higher stream priority, so
         # they take SM slots as soon as K1 CTAs (one frame each) retire and the

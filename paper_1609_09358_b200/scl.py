@@ -241,7 +241,8 @@ def scl_decode_batch(
     nat.check(
         lib.pc_scl_decode(
             nat.ptr(x), B, nat.ptr(queue), nat.ptr(count), dc.ref, ctypes.byref(ncfg), nat.ptr(u), nat.ptr(pw),
-            nat.ptr(mt), nat.ptr(ok), nat.ptr(sel), None, nat.ptr(dc.scl_workspace(ncfg)), nat.stream_handle(stream),
+            nat.ptr(mt), nat.ptr(ok), nat.ptr(sel), None, nat.ptr(dc.new_scl_workspace(ncfg, stream)),
+            nat.stream_handle(stream),
         ),
         "pc_scl_decode",
     )

@@ -313,3 +313,36 @@ def test_crc24_stop_vs_oracle():
     got = bp_decode_batch(llrs, code, BpConfig(i_max=50, stop_mode="crc"))
     late = _check_decisions("crc24", ref_u, ref_it, ref_cv, got, llrs, code)
     print("near-tie frames:", late)
+
+
+@pytest.mark.parametrize("N,mode", [(128, "crc"), (128, "none"), (256, "crc"), (512, "crc")])
+def test_persistent_kernel_matches_per_frame_ctas(N, mode):
+    """pc_bp_cfg_t.work (the frame counter of the persistent kernel at small
+    N) changes scheduling only: bit-identical outputs to one CTA per frame."""
+    import ctypes
+
+    import torch
+    from paper_1609_09358_b200 import _native as nat
+
+    code = CodeConfig(N, N // 2, crc=16)
+    sigma = ebno_to_sigma(2.0, code.rate)
+    B = 3000
+    x = torch.from_numpy(np.array([make_frame(code, sigma, frame_rng(91, N, f))[1] for f in range(B)],
+                                  dtype=np.float32)).cuda()
+    dc = nat.device_code(code)
+    outs = []
+    for use_work in (False, True):
+        cfg = BpConfig(i_max=30, stop_mode=mode).native()
+        wk = torch.full((1,), 12345, dtype=torch.int32, device="cuda")
+        cfg.work = wk.data_ptr() if use_work else None
+        u = torch.zeros((B, N // 32), dtype=torch.int32, device="cuda")
+        su = torch.zeros((B, N), device="cuda")
+        it = torch.zeros(B, dtype=torch.int32, device="cuda")
+        cv = torch.zeros(B, dtype=torch.uint8, device="cuda")
+        nat.check(nat.load().pc_bp_decode(x.data_ptr(), B, dc.ref, ctypes.byref(cfg), u.data_ptr(), None,
+                                          su.data_ptr(), None, it.data_ptr(), cv.data_ptr(), None,
+                                          nat.stream_handle()), "bp")
+        torch.cuda.synchronize()
+        outs.append((u, su, it, cv))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
