@@ -277,12 +277,14 @@ def run_gpu(args):
     prof = ROOT / "profiles" / "bp_kernel_ncu.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            # measured DRAM bytes per frame (one ncu --set full capture) x this launch's frames
+            traffic = json.loads(prof.read_text())["dram_bytes_per_frame"] * dec.chunk
         except Exception:
             traffic = None
     roofline = {
         "bound": "xu", "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
         "traffic": traffic, "kernel": "k_bp2<10,256,0> (register/shuffle BP, TPF=256)",
+        "traffic_source": "profiles/bp_kernel_ncu.json: dram__bytes_read+write per frame x frames per launch",
         "note": "exact-g node updates/s of K1 vs the MUFU (XU) pipe bound: 148 SM x 16 MUFU/clk x sm_max_mhz / "
                 "MUFU per algorithmic g (2nN per frame-iteration, the reference's count; 7 MUFU per PE, 6 in the "
                 "L sweep with kept exponentials, R[n] not computed); HBM is <1% (4.2 KB/frame)",

@@ -1,0 +1,59 @@
+#!/bin/bash
+# Regenerates the round's measured artifacts on a B200 box (run under gpurun):
+#   gpurun --timeout 1800 -- 'bash tools/round_artifacts.sh r01d'
+# then, in the dev container:
+#   bash tools/round_artifacts.sh r01d --summarize
+# Outputs land in gpurun_out/<tag>_*; --summarize copies the judged summaries
+# into profiles/.
+TAG=${1:-rXX}
+OUT=gpurun_out
+if [ "$2" == "--summarize" ]; then
+  for w in c3 c1 c2 c4 c5 ref; do
+    [ -s $OUT/${TAG}_bench_$w.json ] && grep '^{' $OUT/${TAG}_bench_$w.json | tail -1 > profiles/${TAG}_bench_$w.json
+  done
+  cp $OUT/${TAG}_launches.csv profiles/${TAG}_launches.csv
+  python tools/summarize_profiles.py launches $OUT/${TAG}_launches.csv > profiles/${TAG}_launches_summary.txt
+  python tools/summarize_profiles.py full $OUT/${TAG}_bp.ncu-rep \
+    "$TAG: K1 N=1024 (c3 kernel), ncu --set full --clock-control none, tools/profile_kernels.py 16384 256 2.0" \
+    > profiles/${TAG}_ncu_bp.txt
+  python tools/summarize_profiles.py full $OUT/${TAG}_bp4096.ncu-rep \
+    "$TAG: K1 N=4096 (c4 kernel), tools/profile_kernels.py 2048 16 2.0 4096" > profiles/${TAG}_ncu_bp4096.txt
+  python tools/summarize_profiles.py full $OUT/${TAG}_scl.ncu-rep \
+    "$TAG: K3 N=1024 L=32 (c3 kernel), tools/profile_kernels.py 16 4096 1.5" > profiles/${TAG}_ncu_scl.txt
+  tail -3 $OUT/${TAG}_pytest.log > profiles/${TAG}_pytest_gpu.txt
+  python - "$OUT/${TAG}_bp.ncu-rep" "$TAG" <<'PY'
+import csv, io, json, subprocess, sys
+rep, tag = sys.argv[1], sys.argv[2]
+rows = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
+                                                  capture_output=True, text=True).stdout)))
+h, u, r = rows[0], rows[1], rows[2]
+def val(k):
+    v = float(r[h.index(k)].replace(",", ""))
+    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u[h.index(k)], 1)
+frames = 16384
+tot = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+json.dump({"kernel": r[h.index("Kernel Name")], "frames_per_launch": frames, "dram_bytes_per_launch": tot,
+           "dram_bytes_per_frame": tot / frames, "algorithmic_bytes_per_frame": 4173,
+           "source": f"profiles/{tag}_ncu_bp.txt ({tag}_bp.ncu-rep)"},
+          open("profiles/bp_kernel_ncu.json", "w"), indent=1)
+PY
+  exit 0
+fi
+mkdir -p $OUT
+timeout 900 python -m pytest tests -m gpu -q -rf > $OUT/${TAG}_pytest.log 2>&1
+tail -3 $OUT/${TAG}_pytest.log
+timeout 400 python bench.py > $OUT/${TAG}_bench_c3.json 2> $OUT/${TAG}_bench_c3.err
+timeout 400 python bench.py --impl reference > $OUT/${TAG}_bench_ref.json 2> $OUT/${TAG}_bench_ref.err
+for w in c1 c2 c4 c5; do
+  timeout 400 python bench.py --workload $w > $OUT/${TAG}_bench_$w.json 2> $OUT/${TAG}_bench_$w.err
+done
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/${TAG}_launches.csv \
+  python bench.py --steps 1 --warmup 1 --frames 16384 --no-cpu > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_bp2 -c 1 -o $OUT/${TAG}_bp -f \
+  python tools/profile_kernels.py 16384 256 2.0 > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_bp2 -c 1 -o $OUT/${TAG}_bp4096 -f \
+  python tools/profile_kernels.py 2048 16 2.0 4096 > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_scl3 -c 1 -o $OUT/${TAG}_scl -f \
+  python tools/profile_kernels.py 16 4096 1.5 > /dev/null 2>&1
+ls -la $OUT | grep $TAG
+for w in c3 ref c1 c2 c4 c5; do tail -c 400 $OUT/${TAG}_bench_$w.json; echo; done
