@@ -110,6 +110,9 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU baseline --
+_CPU_FRAMES: dict = {}
+
+
 def cpu_hybrid_sample(frames_per_point: int, threads: int):
     """The oracle port (oracle/oracle.c, fp64, the reference's algorithm) on the
     host cores over a bounded sample of the same sweep; returns (Gbit/s, info)."""
@@ -121,8 +124,12 @@ def cpu_hybrid_sample(frames_per_point: int, threads: int):
     bits = 0
     busy = 0.0
     for p, eb in enumerate(EBNO):
-        sigma = ebno_to_sigma(eb, code.rate)
-        llrs = np.array([make_frame(code, sigma, frame_rng(SEED, p, f))[1] for f in range(frames_per_point)])
+        key = (p, frames_per_point)
+        if key not in _CPU_FRAMES:  # host PCG64 frames, generated once per (point, size)
+            sigma = ebno_to_sigma(eb, code.rate)
+            _CPU_FRAMES[key] = np.array([make_frame(code, sigma, frame_rng(SEED, p, f))[1]
+                                         for f in range(frames_per_point)])
+        llrs = _CPU_FRAMES[key]
         t0 = time.perf_counter()
         oracle.hybrid_batch(llrs, code, i_max=IMAX, L=LIST, nthreads=threads)
         busy += time.perf_counter() - t0
@@ -137,7 +144,7 @@ def run_reference(args):
     import oracle
 
     threads = oracle.cpu_count()
-    fpp = args.cpu_frames or max(256, 24 * threads)
+    fpp = args.cpu_frames or max(2048, 128 * threads)  # ~10 s of oracle work on 16 threads
     vals = []
     for s in range(args.warmup + args.steps):
         v, busy = cpu_hybrid_sample(fpp if s >= args.warmup else max(8, threads), threads)
@@ -319,7 +326,7 @@ def run_gpu(args):
         import oracle
 
         threads = oracle.cpu_count()
-        fpp = args.cpu_frames or max(256, 24 * threads)
+        fpp = args.cpu_frames or max(2048, 128 * threads)  # ~10 s of oracle work on 16 threads
         v, busy = cpu_hybrid_sample(fpp, threads)
         cpu = {"value": v, "unit": "Gbit/s", "cores": threads, "kind": "port",
                "sample": f"{fpp} frames per Eb/N0 point x {len(EBNO)} points, {busy:.1f} s of CPU wall "

@@ -160,7 +160,7 @@ def pack_bits(bits: np.ndarray) -> np.ndarray:
 def unpack_bits(words: np.ndarray, L: int) -> np.ndarray:
     w = np.asarray(words, dtype=np.uint32)
     bits = (w[..., :, None] >> np.arange(32, dtype=np.uint32)) & 1
-    return bits.reshape(*w.shape[:-1], -1)[..., :L].astype(np.uint8)
+    return bits.reshape(*w.shape[:-1], w.shape[-1] * 32)[..., :L].astype(np.uint8)
 
 
 class DeviceCode:

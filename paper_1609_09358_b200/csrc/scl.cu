@@ -125,8 +125,13 @@ __global__ void __launch_bounds__(128) k_scl(const SclArgs a)
         if (CH_SMEM) {
             float *mine = chs + grp * N;
             const float *g = a.llr + (size_t)frame * N;
-            for (int t = 4 * pl; t < N; t += 4 * L)
-                *reinterpret_cast<float4 *>(mine + t) = __ldg(reinterpret_cast<const float4 *>(g + t));
+            if (N >= 4) { // rows of N >= 4 floats are 16-byte aligned
+                for (int t = 4 * pl; t < N; t += 4 * L)
+                    *reinterpret_cast<float4 *>(mine + t) = __ldg(reinterpret_cast<const float4 *>(g + t));
+            } else {
+                for (int t = pl; t < N; t += L)
+                    mine[t] = __ldg(g + t);
+            }
             ch = mine;
             __syncwarp();
         } else {
