@@ -5,13 +5,13 @@ For each set: frames whose converged flag or iteration count differ from the
 oracle, split at the reference's iteration 20, and frames where both converged
 but u_hat differs.  Writes a JSON summary.
 
-    python tools/bp_formula_study.py out.json
+    python tests/parity/bp_formula_study.py out.json
 """
 import ctypes
 import json
 import sys
 
-sys.path.insert(0, ".")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[2]))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 

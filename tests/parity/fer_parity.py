@@ -12,7 +12,7 @@ point:
   * the device FER on a larger device-only sample (Philox frames), whose CI
     must overlap the oracle's.
 
-    python tools/fer_parity.py [--frames 2000] [--device-frames 131072] [--out profiles/fer_parity.json]
+    python tests/parity/fer_parity.py [--frames 2000] [--device-frames 131072] [--out profiles/fer_parity.json]
 """
 
 from __future__ import annotations
@@ -27,7 +27,7 @@ from pathlib import Path
 
 import numpy as np
 
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 
 N, K, L, IMAX, SEED = 1024, 512, 32, 50, 31415

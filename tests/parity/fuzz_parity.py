@@ -9,13 +9,13 @@ a batch size and decoder knobs, then checks
 * BP (crc / reencode / none stop): flags, iterations and u_hat identical on
   all but certified near-tie frames (a small fraction; reported).
 
-    python tools/fuzz_parity.py [cases] [seed]
+    python tests/parity/fuzz_parity.py [cases] [seed]
 """
 from __future__ import annotations
 
 import sys
 
-sys.path.insert(0, ".")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[2]))
 import numpy as np  # noqa: E402
 
 import oracle  # noqa: E402

@@ -1,4 +1,4 @@
-"""A fixed slice of the randomized device-vs-oracle sweep (tools/fuzz_parity.py):
+"""A fixed slice of the randomized device-vs-oracle sweep (tests/parity/fuzz_parity.py):
 random codes N = 2..4096 (any rate, CRC none/8/16/24), channel points, batch
 sizes and every decoder knob.  SCL must equal the oracle on every frame
 (except fp64-rounding-limited exact-f frames, certified per frame); BP may
@@ -10,7 +10,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+sys.path.insert(0, str(Path(__file__).resolve().parent / "parity"))
 
 
 @pytest.mark.parametrize("seed", [11, 12])
