@@ -15,7 +15,8 @@ for frames, bb in ((768, 32), (8192, 512), (32768, 4096)):
         for f in range(frames):
             m, l = make_frame(code, sigma, frame_rng(800, 0, f))
             jobs.append(FrameJob(frame_id=f, llrs=l, true_message=m))
-        hybrid_decode_batch(jobs[:64], code, BpConfig(i_max=50), SclConfig(8), bp_batch_size=min(bb,64))
+        # warm-up at the full size (allocations of this capacity happen once)
+        hybrid_decode_batch(jobs, code, BpConfig(i_max=50), SclConfig(8), bp_batch_size=bb)
         st = hybrid_decode_batch(jobs, code, BpConfig(i_max=50), SclConfig(8), bp_batch_size=bb)
         gap = abs(st.t_hyb_theo_bps - st.throughput_bps) / st.t_hyb_theo_bps
         print(frames, bb, eb, f"gamma={st.gamma_bp_fer:.3f} model={st.t_hyb_theo_bps:.3e} measured={st.throughput_bps:.3e} gap={gap*100:.1f}% wall={st.wall_s*1e3:.1f}ms busy={ (st.bp_busy_s+st.scl_busy_s)*1e3:.2f}ms", flush=True)
