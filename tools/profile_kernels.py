@@ -32,6 +32,8 @@ pay = torch.zeros((B, MW), dtype=torch.int32, device="cuda")
 it = torch.zeros(B, dtype=torch.int32, device="cuda")
 cv = torch.zeros(B, dtype=torch.uint8, device="cuda")
 cfg = BpConfig(stop_mode="crc").native()
+work = torch.empty(1, dtype=torch.int32, device="cuda")  # frame counter: the persistent K1 at small N
+cfg.work = work.data_ptr()
 nat.check(lib.pc_bp_decode(llr.data_ptr(), B_BP, dc.ref, ctypes.byref(cfg), None, pay.data_ptr(), None, None,
                            it.data_ptr(), cv.data_ptr(), None, st), "bp")
 scfg = SclConfig(32).native()
