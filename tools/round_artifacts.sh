@@ -48,7 +48,7 @@ for w in c1 c2 c4 c5; do
   timeout 400 python bench.py --workload $w > $OUT/${TAG}_bench_$w.json 2> $OUT/${TAG}_bench_$w.err
 done
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/${TAG}_launches.csv \
-  python bench.py --steps 1 --warmup 1 --frames 16384 --no-cpu > /dev/null 2>&1
+  python bench.py --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_bp2 -c 1 -o $OUT/${TAG}_bp -f \
   python tools/profile_kernels.py 16384 256 2.0 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_bp2 -c 1 -o $OUT/${TAG}_bp4096 -f \
