@@ -5,7 +5,8 @@ Each case draws a code (N = 2..4096, k, CRC none/8/16/24), a channel point,
 a batch size and decoder knobs, then checks
 * SCL (all knobs, DA masks): winners, CRC flags bit-identical to the oracle,
   except frames whose reference winner passes an info position with an fp64
-  leaf LLR below 1e-5 (exact f at high rates: rounding noise in fp64 itself);
+  leaf LLR below fp32 resolution (1e-5, or 4 ulps of the fp32 path metric:
+  `precision_limited`);
 * BP (crc / reencode / none stop): flags, iterations and u_hat identical on
   all but certified near-tie frames (a small fraction; reported).
 
@@ -64,12 +65,19 @@ def sc_leaf_llrs(llr, u, exact_f):
     return out
 
 
-def precision_limited(llr, code, u_ref, exact_f, tol=1e-5):
-    """The reference's winner passes info positions whose fp64 leaf LLR is
-    below fp32 resolution (exact-f chains of high-rate codes reach 0): the
-    decision there is rounding noise in fp64 itself."""
+def precision_limited(llr, code, u_ref, exact_f, metric_ref=0.0):
+    """The reference's winner passes an info position whose fp64 leaf LLR is
+    below fp32 resolution: below 1e-5 (exact-f chains of high-rate codes reach
+    0, rounding noise in fp64 itself), or below 4 ulps of the fp32 path metric
+    (the two children's metrics differ by |leaf LLR|, so a smaller margin
+    cannot be resolved by an fp32 metric of that size)."""
+    tol = max(1e-5, 4.0 * float(np.spacing(np.float32(abs(metric_ref)))))
     leaves = sc_leaf_llrs(llr, u_ref, exact_f)
     return bool(np.abs(leaves[np.asarray(code.info_positions)]).min() < tol)
+
+
+SCL_CERTIFIED = 0
+SCL_FRAMES = 0
 
 
 def scl_case(rng, seed):
@@ -79,17 +87,26 @@ def scl_case(rng, seed):
                     selector=str(rng.choice(["pseudo", "bitonic"])),
                     da_threshold=float(rng.choice([0.0, 0.0, 0.3])))
     B = int(rng.integers(1, 40 if code.N <= 1024 else 8))
-    llrs = frames(code, float(rng.uniform(-1.0, 4.0)), B, seed)
+    eb = float(rng.uniform(-1.0, 4.0))
+    llrs = frames(code, eb, B, seed)
     got = scl_decode_batch(llrs, code, cfg)
     da = decision_aided_mask(code, cfg.da_threshold) if cfg.da_threshold > 0 else None
     bad = []
+    global SCL_CERTIFIED, SCL_FRAMES
+    SCL_FRAMES += B
     for f in range(B):
         ref = oracle.scl_decode(llrs[f], code, L, da=da, metric_mode=cfg.metric_mode, f_mode=cfg.f_mode,
                                 selector=cfg.selector)
         if not (np.array_equal(got.u_hat[f], ref["u_hat"]) and bool(got.crc_ok[f]) == ref["crc_ok"]):
-            if not precision_limited(llrs[f], code, ref["u_hat"], cfg.f_mode == "exact"):
+            if precision_limited(llrs[f], code, ref["u_hat"], cfg.f_mode == "exact", ref["metric"]):
+                SCL_CERTIFIED += 1
+            else:
                 bad.append(f)
-    return f"SCL N={code.N} k={code.k} crc={code.crc.width if code.crc else None} {cfg} B={B}", bad, B
+                leaves = sc_leaf_llrs(llrs[f], ref["u_hat"], cfg.f_mode == "exact")
+                print(f"  frame {f}: min |fp64 leaf| on info = {np.abs(leaves[np.asarray(code.info_positions)]).min():.3e}, "
+                      f"metric dev {float(got.metric[f]):.6f} ref {ref['metric']:.6f}", flush=True)
+    return (f"SCL N={code.N} k={code.k} crc={code.crc.width if code.crc else None} {cfg} B={B} eb={eb!r} "
+            f"frame_seed={seed}"), bad, B
 
 
 def bp_case(rng, seed):
@@ -131,5 +148,6 @@ if __name__ == "__main__":
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     s = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     fails, scl_bad, bp_diff, bp_frames = run(n, s)
-    print(f"SCL frames differing: {scl_bad}; BP frames differing (near-tie class): {bp_diff}/{bp_frames}")
+    print(f"SCL frames differing: {scl_bad}; certified precision-limited: {SCL_CERTIFIED}/{SCL_FRAMES}; "
+          f"BP frames differing (near-tie class): {bp_diff}/{bp_frames}")
     sys.exit(1 if fails else 0)
