@@ -502,37 +502,43 @@ def run_bp_workload(args):
         host[p].copy_(llr[p])
     pay_h = [torch.empty((B, MW), dtype=torch.int32, pin_memory=True) for _ in pts]
     conv_h = [torch.empty(B, dtype=torch.uint8, pin_memory=True) for _ in pts]
-    dbufs = [torch.empty((B, n4), dtype=torch.float32, device=dev) for _ in range(2)]
+    # e2e units: each point's batch in NC chunks, NBUF chunk buffers, so the
+    # first exposed copy is one chunk and the link streams ahead of the decode
+    NC, NBUF = (4, 3) if B % 4 == 0 else (1, 2)
+    Bc = B // NC
+    dbufs = [torch.empty((Bc, n4), dtype=torch.float32, device=dev) for _ in range(NBUF)]
     s_copy = torch.cuda.Stream(device=dev)
 
     def e2e_run(nsteps):
-        # one stream of host batches (nsteps x points): the H2D of batch i+1 on a
-        # copy stream overlaps the decode of batch i
         cur = torch.cuda.current_stream(dev)
-        seq = [p for _ in range(nsteps) for p in range(len(pts))]
-        h2d, done = [], []
+        seq = [(p, c) for _ in range(nsteps) for p in range(len(pts)) for c in range(NC)]
+        h2d, done = [None] * len(seq), [None] * len(seq)
 
         def issue(i):
+            p, c = seq[i]
             with torch.cuda.stream(s_copy):
-                if i >= 2:
-                    s_copy.wait_event(done[i - 2])
-                dbufs[i % 2].copy_(host[seq[i]], non_blocking=True)
+                if i >= NBUF:
+                    s_copy.wait_event(done[i - NBUF])
+                dbufs[i % NBUF].copy_(host[p][c * Bc:(c + 1) * Bc], non_blocking=True)
                 e = torch.cuda.Event()
                 e.record(s_copy)
-                h2d.append(e)
+                h2d[i] = e
 
-        issue(0)
-        for i, p in enumerate(seq):
-            if i + 1 < len(seq):
-                issue(i + 1)
+        for i in range(min(NBUF - 1, len(seq))):
+            issue(i)
+        for i, (p, c) in enumerate(seq):
+            if i + NBUF - 1 < len(seq):
+                issue(i + NBUF - 1)
             cur.wait_event(h2d[i])
-            nat.check(lib.pc_bp_decode(dbufs[i % 2].data_ptr(), B, dc.ref, ctypes.byref(cfg), None, pay.data_ptr(),
-                                       None, None, iters[p].data_ptr(), conv[p].data_ptr(), None, st), "pc_bp_decode")
+            nat.check(lib.pc_bp_decode(dbufs[i % NBUF].data_ptr(), Bc, dc.ref, ctypes.byref(cfg), None,
+                                       pay.data_ptr() + 4 * MW * c * Bc, None, None, iters[p].data_ptr() + 4 * c * Bc,
+                                       conv[p].data_ptr() + c * Bc, None, st), "pc_bp_decode")
             e = torch.cuda.Event()
             e.record(cur)
-            done.append(e)
-            pay_h[p].copy_(pay, non_blocking=True)
-            conv_h[p].copy_(conv[p], non_blocking=True)
+            done[i] = e
+            if c == NC - 1:  # the point's payloads and flags back to the host
+                pay_h[p].copy_(pay, non_blocking=True)
+                conv_h[p].copy_(conv[p], non_blocking=True)
         torch.cuda.synchronize()
 
     fixed = None

@@ -210,8 +210,8 @@ class HybridDecoder:
 
     def decode_host_many(self, batches):
         """End-to-end call over several HOST batches (pinned float32 [B_i, N]):
-        the H2D copy of batch i+1 runs on a copy stream while batch i decodes
-        (two device input buffers), and each batch's payload words and converged
+        the H2D copies of batches i+1 and i+2 run on a copy stream while batch i
+        decodes (three device input buffers), and each batch's payload words and converged
         flags are read back on the copy stream while the next batch decodes.  Returns a list of
         (payload words uint32 [B_i, ceil(m/32)], converged bool [B_i]) numpy
         arrays, in order: views of pinned buffers that the next call reuses (copy
@@ -224,8 +224,12 @@ class HybridDecoder:
             if b.shape[0] > self.capacity:
                 raise ValueError(f"batch of {b.shape[0]} frames exceeds capacity {self.capacity}")
         N = self.code.N
+        # NBUF device input buffers: the copy of batch i+NBUF-1 starts while
+        # batch i decodes, so the link keeps copying through short decodes
+        # (a fast point's decode can be shorter than its PCIe copy).
+        NBUF = 3
         if getattr(self, "_dbuf", None) is None or self._dbuf[0].shape[0] < self.capacity:
-            self._dbuf = [torch.empty((self.capacity, N), dtype=torch.float32, device=dev) for _ in range(2)]
+            self._dbuf = [torch.empty((self.capacity, N), dtype=torch.float32, device=dev) for _ in range(NBUF)]
             self._s_copy = torch.cuda.Stream(device=dev)
         cur = torch.cuda.current_stream(dev)
         outs = []
@@ -233,10 +237,10 @@ class HybridDecoder:
         done = [None] * len(batches)
 
         def issue_h2d(i):
-            buf = self._dbuf[i % 2]
+            buf = self._dbuf[i % NBUF]
             with torch.cuda.stream(self._s_copy):
-                if i >= 2:  # the buffer is free once batch i-2 has decoded
-                    self._s_copy.wait_event(done[i - 2])
+                if i >= NBUF:  # the buffer is free once batch i-NBUF has decoded
+                    self._s_copy.wait_event(done[i - NBUF])
                 buf[: batches[i].shape[0]].copy_(batches[i], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(self._s_copy)
@@ -250,16 +254,17 @@ class HybridDecoder:
                                        chunk=self.chunk, overlap=self.overlap, device=self.device)
         decs = (self, self._twin)
         d2h = [None] * len(batches)
-        issue_h2d(0)
+        for i in range(min(NBUF - 1, len(batches))):
+            issue_h2d(i)
         for i, b in enumerate(batches):
-            if i + 1 < len(batches):
-                issue_h2d(i + 1)
+            if i + NBUF - 1 < len(batches):
+                issue_h2d(i + NBUF - 1)  # its buffer held batch i-1, decoded already (in stream order)
             B = int(b.shape[0])
             dec = decs[i % 2]
             cur.wait_event(h2d[i])
             if i >= 2:  # batch i-2's results (same decoder) have been copied out
                 cur.wait_event(d2h[i - 2])
-            dec.run(self._dbuf[i % 2][:B], B)
+            dec.run(self._dbuf[i % NBUF][:B], B)
             ev = torch.cuda.Event()
             ev.record(cur)
             done[i] = ev
