@@ -504,7 +504,7 @@ def run_bp_workload(args):
     conv_h = [torch.empty(B, dtype=torch.uint8, pin_memory=True) for _ in pts]
     # e2e units: each point's batch in NC chunks, NBUF chunk buffers, so the
     # first exposed copy is one chunk and the link streams ahead of the decode
-    NC, NBUF = (4, 3) if B % 4 == 0 else (1, 2)
+    NC, NBUF = (4, 3) if B % 4 == 0 else (1, 2)  # (8 chunks measured slower: launch tails)
     Bc = B // NC
     dbufs = [torch.empty((Bc, n4), dtype=torch.float32, device=dev) for _ in range(NBUF)]
     s_copy = torch.cuda.Stream(device=dev)
