@@ -63,6 +63,22 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def spawn_ranks(n: int) -> int:
+    """``--gpus N`` without a launcher: re-run this script as N ranks under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1).
+    Rank 0 prints the JSON line; torchrun's exit code is returned."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
@@ -250,17 +266,19 @@ def run_gpu(args):
         nat.check(lib.pc_count_errors(dec.payload.data_ptr(), msg[p].data_ptr(), B, m, errs[p].data_ptr(),
                                       nat.stream_handle()), "pc_count_errors")
     torch.cuda.synchronize()
-    if world > 1:  # whole-job statistics: sum the per-rank counters (off the timed path)
-        stats = torch.tensor([[iters_sum[p], round(gammas[p] * B)] for p in range(len(EBNO))], dtype=torch.int64,
-                             device=COMM)
+    # whole-job statistics: exact integer counters summed over the ranks (off
+    # the timed path); the roofline below uses this rank's own iterations and
+    # its own K1 time
+    local_iters = list(iters_sum)
+    stats = torch.tensor([[iters_sum[p], round(gammas[p] * B), int(errs[p, 0]), int(errs[p, 1])]
+                          for p in range(len(EBNO))], dtype=torch.int64, device=COMM)
+    if world > 1:
         dist.all_reduce(stats)
-        errs_c = errs.to(COMM)
-        dist.all_reduce(errs_c)
-        errs = errs_c.to(dev)
-        for p in range(len(EBNO)):
-            iters_sum[p] = int(stats[p, 0]) / world  # per-rank average keeps the per-GPU roofline arithmetic
-            gammas[p] = float(stats[p, 1]) / (B * world)
-    errs_h = errs.cpu().numpy()
+    stats = stats.cpu().numpy()
+    errs_h = stats[:, 2:4]
+    for p in range(len(EBNO)):
+        iters_sum[p] = int(stats[p, 0])
+        gammas[p] = float(stats[p, 1]) / (B * world)
 
     max_ms = max_over_ranks(elapsed_ms, device=COMM)
     bits_step = B * m * len(EBNO)
@@ -268,7 +286,7 @@ def run_gpu(args):
 
     # ---- roofline of the dominant kernel (K1): algorithmic exact-g evaluations / K1 time ----
     n = code.n
-    g_per_step = sum(iters_sum) * 2 * n * N  # iterations are deterministic per input set
+    g_per_step = sum(local_iters) * 2 * n * N  # iterations are deterministic per input set
     bp_ms_step = sum(bp_ms) / args.steps
     achieved = g_per_step / (bp_ms_step * 1e-3) / 1e9  # Gg/s
     ck = clocks.summary()
@@ -336,9 +354,10 @@ def run_gpu(args):
     for p, eb in enumerate(EBNO):
         ms = pt_ms[p] / args.steps
         sweep.append({"ebno_db": eb, "gbps": B * m / (ms * 1e-3) / 1e9 * world, "ms": ms, "gamma": gammas[p],
-                      "mean_bp_iters": iters_sum[p] / B, "p50_latency_ms": lat_p50[p],
+                      "mean_bp_iters": iters_sum[p] / (B * world), "p50_latency_ms": lat_p50[p],
                       "fer": float(errs_h[p, 1]) / (B * world), "ber": float(errs_h[p, 0]) / (B * m * world),
-                      "frames": B * world})
+                      "frames": B * world, "frame_errors": int(errs_h[p, 1]), "bit_errors": int(errs_h[p, 0]),
+                      "frames_to_scl": int(stats[p, 1]), "bp_iterations": int(stats[p, 0])})
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
@@ -374,6 +393,11 @@ def _gpu_common(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    # NCCL's INIT log (one "Init COMPLETE" per rank) goes to stderr, so the rank
+    # count of a run is visible; the JSON line on stdout stays alone
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     ngpu = torch.cuda.device_count()
     local = local % max(1, ngpu)
     torch.cuda.set_device(local)
@@ -488,8 +512,13 @@ def run_bp_workload(args):
                                    None, iters[p].data_ptr(), conv[p].data_ptr(), None, st), "pc_bp_decode")
         nat.check(lib.pc_count_errors(pay.data_ptr(), msg[p].data_ptr(), B, m, errs[p].data_ptr(), st), "count")
     torch.cuda.synchronize()
-    it_sum = iters.to(torch.int64).sum(dim=1).cpu().numpy()
-    errs_h = errs.cpu().numpy()
+    it_local = iters.to(torch.int64).sum(dim=1)
+    # exact whole-job counters: iterations, bit errors, frame errors, BP failures summed over ranks
+    stats = torch.stack([it_local, errs[:, 0], errs[:, 1], (conv == 0).to(torch.int64).sum(dim=1)], dim=1).to(COMM)
+    if world > 1:
+        dist.all_reduce(stats)
+    stats = stats.cpu().numpy()
+    it_sum = it_local.cpu().numpy()  # this rank's, for its own roofline
     max_ms = max_over_ranks(ms, device=COMM)
     value = world * B * m * len(pts) * args.steps / (max_ms * 1e-3) / 1e9
     g_step = int(it_sum.sum()) * 2 * code.n * n4
@@ -605,8 +634,11 @@ def run_bp_workload(args):
                        "parallelism": f"frame-sharded x{world}",
                        "l2": f"inputs larger than L2 ({B * n4 * 4 / 1e6:.0f} MB per point)"},
             "sweep": [{"ebno_db": eb, "gbps": world * B * m / (pt_ms[p] * 1e-3) / 1e9, "ms": pt_ms[p],
-                       "mean_bp_iters": float(it_sum[p]) / B, "fer": float(errs_h[p, 1]) / B,
-                       "ber": float(errs_h[p, 0]) / (B * m)} for p, eb in enumerate(pts)],
+                       "mean_bp_iters": float(stats[p, 0]) / (B * world), "fer": float(stats[p, 2]) / (B * world),
+                       "ber": float(stats[p, 1]) / (B * m * world), "frames": B * world,
+                       "bp_iterations": int(stats[p, 0]), "bit_errors": int(stats[p, 1]),
+                       "frame_errors": int(stats[p, 2]), "bp_failures": int(stats[p, 3])}
+                      for p, eb in enumerate(pts)],
             "roofline": {"bound": "xu", "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
                          "traffic": None, "kernel": wl["kernel"],
                          "note": "exact-g node updates/s (2nN per frame-iteration) vs 148 SM x 16 MUFU/clk / "
@@ -714,11 +746,15 @@ def run_scl_workload(args):
                 b1.record()
                 torch.cuda.synchronize()
                 one.append(a1.elapsed_time(b1))
-            e = errs[li].cpu().numpy()
+            e_t = errs[li].to(COMM)
+            if world > 1:  # whole-job error counters
+                dist.all_reduce(e_t)
+            e = e_t.cpu().numpy()
             rows.append({"L": L, "ebno_db": eb, "ms_per_batch": ms, "frames_per_s": world * B / (ms * 1e-3),
                          "gbps": world * B * m / (ms * 1e-3) / 1e9, "batch_p50_latency_ms": p50,
-                         "single_frame_latency_ms": float(np.median(one[5:])), "fer": float(e[1]) / B,
-                         "ber": float(e[0]) / (B * m)})
+                         "single_frame_latency_ms": float(np.median(one[5:])), "fer": float(e[1]) / (B * world),
+                         "ber": float(e[0]) / (B * m * world), "frames": B * world, "frame_errors": int(e[1]),
+                         "bit_errors": int(e[0])})
     if rank == 0:
         cpu = None
         if not args.no_cpu:
@@ -773,6 +809,8 @@ def main():
                     help="c3 = hybrid sweep (headline); c1 = BP N=128; c2 = SCL N=1024 L=32 sweep; "
                          "c4 = BP N=4096; c5 = SCL N=2048 list-size sweep")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload in BP_WORKLOADS:

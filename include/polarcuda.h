@@ -53,14 +53,27 @@ typedef struct pc_code {
     int32_t crc_width;           /* 0 (no CRC), 8, 16 or 24 */
     uint32_t crc_offset;         /* CRC register after k zero bits (0 for init = 0) */
     uint32_t enc_crc_offset;     /* CRC register after m zero bits */
-    int32_t first_info;          /* info_pos[0] (host copy): SCL decodes the all-frozen prefix
-                                    before it element-parallel; 0 disables that path */
+    int32_t first_info;          /* info_pos[0], DERIVED by pc_code_seal (SCL decodes the
+                                    all-frozen prefix before it element-parallel) */
     const uint32_t *frozen_bits; /* [ceil(N/32)]  1 = frozen                      */
     const uint32_t *crc_cols;    /* [N] register contribution of a 1 at position i */
     const int32_t *info_pos;     /* [k] ascending non-frozen positions             */
     const uint32_t *enc_cols;    /* [m] register contribution of payload bit j     */
     const uint32_t *da_bits;     /* [ceil(N/32)] decision-aided positions or NULL  */
+    uint64_t seal;               /* written by pc_code_seal; every decode call checks it */
 } pc_code_t;
+
+/* Validate a code's device tables and seal the struct (call once after filling
+ * it, before any decode; synchronous on `stream`).  Reads frozen_bits, info_pos
+ * and da_bits back and checks: N - k frozen positions; info_pos = the
+ * non-frozen positions in ascending order; decision-aided positions are not
+ * frozen.  Then DERIVES first_info = info_pos[0] (the caller's value is
+ * ignored) and writes `seal`, a hash of every field.  pc_bp_decode,
+ * pc_bp_iterate, pc_scl_decode, pc_encode and pc_gen_frames return
+ * PC_ERR_INVALID for a struct that was never sealed or was changed after
+ * sealing (e.g. a hand-set first_info), instead of decoding with it.
+ * Mirrors the validation of CodeConfig.__init__ (polar.py:235-263). */
+int pc_code_seal(pc_code_t *code, void *stream);
 
 /* BpConfig, bp.py:40-57.  g_mode 0 = exact, 1 = min, 2 = exact evaluated per g
  * (4 MUFU, the pre-exponential-domain form; N = 1024/2048, parity studies); stop_mode 0 = crc,

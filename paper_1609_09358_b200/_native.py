@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+from collections import OrderedDict
 from pathlib import Path
 
 import numpy as np
@@ -22,6 +23,7 @@ PC_OK = 0
 EXPORTS = (
     "pc_version",
     "pc_strerror",
+    "pc_code_seal",
     "pc_workspace_bytes",
     "pc_device_count",
     "pc_bp_decode",
@@ -51,6 +53,7 @@ class PcCode(C.Structure):
         ("info_pos", C.c_void_p),
         ("enc_cols", C.c_void_p),
         ("da_bits", C.c_void_p),
+        ("seal", C.c_uint64),
     ]
 
 
@@ -99,6 +102,7 @@ def load():
     sig = {
         "pc_version": (i32, []),
         "pc_strerror": (C.c_char_p, [i32]),
+        "pc_code_seal": (i32, [vp, vp]),
         "pc_workspace_bytes": (i64, []),
         "pc_device_count": (i32, []),
         "pc_bp_decode": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
@@ -192,13 +196,15 @@ class DeviceCode:
             code.crc_width,
             off,
             eoff,
-            int(code.info_positions[0]) if code.k > 0 else 0,
+            0,  # first_info: derived by pc_code_seal
             ptr(self.frozen_bits),
             ptr(self.crc_cols),
             ptr(self.info_pos),
             ptr(self.enc_cols),
             ptr(self.da_bits),
         )
+        # the library validates the device tables, derives first_info and seals the struct
+        check(load().pc_code_seal(C.byref(self.struct), stream_handle()), "pc_code_seal")
         self.workspace = torch.zeros(max(1, load().pc_workspace_bytes() // 4), dtype=torch.int32, device=dev)
 
     @property
@@ -242,24 +248,29 @@ class DeviceCode:
         return DeviceCode(self.code, self.device, da_mask)
 
 
-_CODE_CACHE: dict = {}
+_CODE_CACHE: "OrderedDict" = OrderedDict()
+_CODE_CACHE_MAX = 16  # device tables of the most recently used codes (a sweep builds a CodeConfig per point)
+
+
+def _cached(key, code, make):
+    dc = _CODE_CACHE.get(key)
+    if dc is None or dc.code is not code:  # (an id() reused by a new CodeConfig is a miss)
+        dc = make()
+        _CODE_CACHE[key] = dc
+    _CODE_CACHE.move_to_end(key)
+    while len(_CODE_CACHE) > _CODE_CACHE_MAX:
+        _CODE_CACHE.popitem(last=False)  # holders (decoders) keep their own reference
+    return dc
 
 
 def device_code(code, da_mask=None) -> DeviceCode:
     import torch
 
     key = (id(code), torch.cuda.current_device())
-    dc = _CODE_CACHE.get(key)
-    if dc is None or dc.code is not code:
-        dc = DeviceCode(code)
-        _CODE_CACHE[key] = dc
+    dc = _cached(key, code, lambda: DeviceCode(code))
     if da_mask is not None and np.any(da_mask):
         dkey = key + (pack_bits(np.asarray(da_mask, np.uint8)).tobytes(),)
-        dd = _CODE_CACHE.get(dkey)
-        if dd is None or dd.code is not code:
-            dd = DeviceCode(code, dc.device, da_mask)
-            _CODE_CACHE[dkey] = dd
-        return dd
+        return _cached(dkey, code, lambda: DeviceCode(code, dc.device, da_mask))
     return dc
 
 

@@ -230,6 +230,7 @@ def bp_decode_batch(
     dev = x.device
     NW = (code.N + 31) // 32
     MW = (code.message_len + 31) // 32
+    cur = torch.cuda.current_stream(dev)
     u = torch.empty((B, NW), dtype=torch.int32, device=dev)
     it = torch.empty(B, dtype=torch.int32, device=dev)
     cv = torch.empty(B, dtype=torch.uint8, device=dev)
@@ -239,9 +240,9 @@ def bp_decode_batch(
     dc = nat.device_code(code)
     ncfg = cfg.native()
     wk = torch.empty(1, dtype=torch.int32, device=dev)  # frame counter of the persistent kernel (small N)
-    if stream is not None:
-        wk.record_stream(stream)  # freed to the caching allocator only after the launch on `stream`
     ncfg.work = wk.data_ptr()
+    if stream is not None:  # the launch stream sees the input converted on the current stream
+        stream.wait_stream(cur)
     nat.check(
         lib.pc_bp_decode(
             nat.ptr(x), B, dc.ref, C_byref(ncfg), nat.ptr(u), nat.ptr(pw), nat.ptr(su), nat.ptr(sx),
@@ -249,6 +250,11 @@ def bp_decode_batch(
         ),
         "pc_bp_decode",
     )
+    if stream is not None:  # results are read on the current stream; temporaries outlive the launch
+        for t in (x, u, it, cv, su, sx, pw, wk):
+            if t is not None:
+                t.record_stream(stream)
+        cur.wait_stream(stream)
     if not host:
         return BpBatchResult(u, cv.bool(), it, su, sx, pw)
     ub = nat.unpack_bits(u.cpu().numpy().view(np.uint32), code.N)
@@ -272,7 +278,7 @@ def bp_decode(llrs: np.ndarray, code: CodeConfig, cfg: BpConfig | None = None) -
     r = bp_decode_batch(llrs[None, :], code, cfg, soft=True)
     su, sx = r.soft_u[0], r.soft_x[0]
     return BpResult(
-        u_hat=_hard(su),
+        u_hat=r.u_hat[0].copy(),  # the kernel's own decisions (the batch API's u_hat)
         x_hat=_hard(sx),
         soft_u=su,
         soft_x=sx,

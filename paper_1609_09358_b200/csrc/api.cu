@@ -1,9 +1,29 @@
 // api.cu -- the C-ABI (include/polarcuda.h): validation, then the launchers.
 #include "args.cuh"
 
+#include <vector>
+
 using namespace pc;
 
-static int check_code(const pc_code_t *c)
+// Hash of every field a kernel reads (not the seal itself), salted so that a
+// zero-filled struct never carries a valid seal.
+static uint64_t seal_of(const pc_code_t *c)
+{
+    uint64_t h = 0xcbf29ce484222325ull ^ 0x706f6c6172637564ull;
+    auto mix = [&h](uint64_t v) {
+        for (int i = 0; i < 8; ++i) {
+            h ^= (v >> (8 * i)) & 0xffu;
+            h *= 0x100000001b3ull;
+        }
+    };
+    mix((uint32_t)c->N), mix((uint32_t)c->n), mix((uint32_t)c->k), mix((uint32_t)c->m);
+    mix((uint32_t)c->crc_width), mix(c->crc_offset), mix(c->enc_crc_offset), mix((uint32_t)c->first_info);
+    mix((uintptr_t)c->frozen_bits), mix((uintptr_t)c->crc_cols), mix((uintptr_t)c->info_pos);
+    mix((uintptr_t)c->enc_cols), mix((uintptr_t)c->da_bits);
+    return h | 1u;
+}
+
+static int check_shape(const pc_code_t *c)
 {
     if (c == nullptr || c->N < 2 || c->n < 1 || c->n > PC_MAX_LOGN || (1 << c->n) != c->N)
         return PC_ERR_INVALID;
@@ -18,9 +38,60 @@ static int check_code(const pc_code_t *c)
     return PC_OK;
 }
 
+static int check_code(const pc_code_t *c)
+{
+    const int rc = check_shape(c);
+    if (rc)
+        return rc;
+    return c->seal == seal_of(c) ? PC_OK : PC_ERR_INVALID; // never sealed, or changed since
+}
+
 extern "C" {
 
 int pc_version(void) { return 1; }
+
+int pc_code_seal(pc_code_t *code, void *stream)
+{
+    if (code == nullptr)
+        return PC_ERR_INVALID;
+    code->first_info = 0; // derived below; the shape check must not depend on the caller's value
+    int rc = check_shape(code);
+    if (rc)
+        return rc;
+    const int N = code->N, k = code->k, NW = (N + 31) / 32;
+    std::vector<uint32_t> fz(NW), da;
+    std::vector<int32_t> ip(k);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemcpyAsync(fz.data(), code->frozen_bits, NW * sizeof(uint32_t), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(ip.data(), code->info_pos, k * sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return PC_ERR_CUDA;
+    if (code->da_bits != nullptr) {
+        da.resize(NW);
+        if (cudaMemcpyAsync(da.data(), code->da_bits, NW * sizeof(uint32_t), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess)
+            return PC_ERR_CUDA;
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess)
+        return PC_ERR_CUDA;
+    int nfrozen = 0, j = 0;
+    for (int i = 0; i < N; ++i) {
+        if ((fz[i >> 5] >> (i & 31)) & 1u) {
+            ++nfrozen;
+            if (!da.empty() && ((da[i >> 5] >> (i & 31)) & 1u))
+                return PC_ERR_INVALID; // a decision-aided position must carry information
+        } else {
+            if (j >= k || ip[j] != i)
+                return PC_ERR_INVALID; // info_pos must list the non-frozen positions in order
+            ++j;
+        }
+    }
+    if (nfrozen != N - k || j != k)
+        return PC_ERR_INVALID;
+    code->first_info = ip[0];
+    code->seal = seal_of(code);
+    return PC_OK;
+}
 
 const char *pc_strerror(int code)
 {
@@ -155,7 +226,7 @@ int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32
 
 int64_t pc_scl_workspace_bytes(const pc_code_t *code, const pc_scl_cfg_t *cfg)
 {
-    if (check_code(code) || cfg == nullptr || cfg->L < 1 || cfg->L > PC_MAX_LIST || (cfg->L & (cfg->L - 1)))
+    if (check_shape(code) || cfg == nullptr || cfg->L < 1 || cfg->L > PC_MAX_LIST || (cfg->L & (cfg->L - 1)))
         return -1;
     SclArgs a{};
     a.code = to_device_code(*code);

@@ -18,7 +18,8 @@ __global__ void k_compact(const uint8_t *__restrict__ conv, int B, int32_t *queu
     int base = 0;
     if (lane == leader)
         base = atomicAdd(count, __popc(m));
-    base = __shfl_sync(m | (1u << leader), base, leader);
+    // every lane of the warp reaches this point (the m == 0 exit above is warp-uniform)
+    base = __shfl_sync(0xffffffffu, base, leader);
     if (fail)
         queue[base + __popc(m & ((1u << lane) - 1u))] = b;
 }

@@ -497,6 +497,29 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 a.soft_x[(size_t)f * N + i2] = (Lch[i2] + o2) * KOUT;
             }
         }
+    } else {
+        // BW = n (one warp per frame at N = 128): R[n-1] is a register stage, so
+        // R[n] comes from the same lane-pair exchange as the R sweep's boundary n
+        if (a.soft_x != nullptr) {
+            constexpr int j = LOGN;
+            const int msk = 1 << (j - 1 - B);
+            const bool hi = lane & msk;
+#pragma unroll
+            for (int k = 0; k < Q / 2; ++k) {
+                const float Rk = RGET(j - 1, k), Rh = RGET(j - 1, k + Q / 2);
+                const float Lk = LGET(j, k), Lh = LGET(j, k + Q / 2);
+                const float pr = __shfl_xor_sync(0xffffffffu, hi ? Rk : Rh, msk);
+                const float pl = __shfl_xor_sync(0xffffffffu, hi ? Lk : Lh, msk);
+                const float myR = hi ? Rh : Rk, myL = hi ? Lh : Lk;
+                const float av = hi ? pr : myR, r2v = hi ? myR : pr, l1 = hi ? pl : myL, l2 = hi ? myL : pl;
+                float o1, o2;
+                bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                const float back = __shfl_xor_sync(0xffffffffu, hi ? o1 : o2, msk);
+                const float rk = hi ? back : o1, rh = hi ? o2 : back; // R[n] at my nodes k, k + Q/2
+                a.soft_x[(size_t)f * N + base + k] = (Lk + rk) * KOUT;
+                a.soft_x[(size_t)f * N + base + k + Q / 2] = (Lh + rh) * KOUT;
+            }
+        }
     }
     __syncthreads();
     // bit-pack with warp ballots: thread b of the pass owns bit b (coalesced
@@ -611,16 +634,17 @@ static int launch_bp2_n(const BpArgs &a, int tpf, cudaStream_t s)
 }
 
 // K1 v2 covers N = 128 .. 4096 with every stop rule (re-encode: TPF >= 64) and
-// soft_x at N = 4096 (below, the shared-memory kernel in bp.cu forms it).
+// both soft outputs; the shared-memory kernel in bp.cu serves N < 128, the
+// re-encode stop at TPF = 32 and the kernel = 1 knob.
 // N = 4096 runs one 512-thread CTA per frame (Q = 8): 9 shared rows (144 KB),
 // no kept exponentials, one CTA per SM.
 bool bp2_eligible(const BpArgs &a, int tpf)
 {
     const int N = a.code.N;
     const int lo = N / 8 > 32 ? N / 8 : 32;
-    // soft_x only where the smem kernel (bp.cu) has no room: N = 4096
-    if (!(a.code.n >= 7 && a.code.n <= 12 && (a.soft_x == nullptr || a.code.n == 12) &&
-          (tpf <= 0 || (tpf >= lo && tpf <= N / 2))))
+    // soft outputs at every N: bp_decode (per frame, soft_u and soft_x) and
+    // bp_decode_batch / the hybrid run the same kernel, so they decide alike
+    if (!(a.code.n >= 7 && a.code.n <= 12 && (tpf <= 0 || (tpf >= lo && tpf <= N / 2))))
         return false;
     if (a.stop_mode != 1)
         return true;

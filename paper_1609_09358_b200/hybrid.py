@@ -300,10 +300,20 @@ class HybridDecoder:
         """Enqueue the pipeline for ``llr[:B]`` (CUDA float32).  Returns immediately;
         call ``sync()`` (or read results) afterwards."""
         torch = self.torch
+        N = self.code.N
+        if not (hasattr(llr, "is_cuda") and llr.is_cuda):
+            raise ValueError("HybridDecoder.run takes a CUDA tensor (use decode_host for host buffers)")
+        if llr.dtype != torch.float32 or llr.dim() != 2 or llr.shape[1] != N:
+            raise ValueError(f"expected float32 llrs of shape (B, {N}), got {llr.dtype} {tuple(llr.shape)}")
+        if llr.device != self.device:
+            raise ValueError(f"llrs are on {llr.device}, the decoder on {self.device}")
+        if not llr.is_contiguous() or llr.data_ptr() % 16:
+            raise ValueError("llrs must be contiguous and 16-byte aligned (TMA row copies)")
         B = int(llr.shape[0] if B is None else B)
+        if B > llr.shape[0] or B < 0:
+            raise ValueError(f"B={B} outside the {llr.shape[0]} rows of llrs")
         if B > self.capacity:
             raise ValueError(f"batch of {B} frames exceeds capacity {self.capacity}")
-        N = self.code.N
         lib, chk = self.lib, nat.check
         cur = torch.cuda.current_stream(self.device)
         self.s_bp.wait_stream(cur)
@@ -383,13 +393,16 @@ def hybrid_decode_batch(
     bp_batch_size: int = 32,
     n_scl_workers: int = 2,
     buffer_capacity: int | None = None,
+    decoder: "HybridDecoder | None" = None,
 ) -> HybridStats:
     """Decode jobs through the device pipeline; jobs are completed in place.
 
     ``bp_batch_size`` is the chunk that shares one BP service interval, as in
     the reference; ``n_scl_workers`` and ``buffer_capacity`` are validated for
     API compatibility (the device queue of a chunk always holds all of its
-    failures, so it can neither drop nor block).
+    failures, so it can neither drop nor block).  ``decoder`` reuses a
+    ``HybridDecoder`` of the same code across calls (a sweep point's chunks);
+    its capacity must hold the jobs and its chunk must equal ``bp_batch_size``.
     """
     if not jobs:
         raise ValueError("no jobs to decode")
@@ -404,7 +417,16 @@ def hybrid_decode_batch(
     llr_host = np.stack([np.asarray(j.llrs, dtype=np.float64) for j in jobs])
     if llr_host.shape[1] != code.N:
         raise ValueError(f"expected {code.N} channel LLRs per job, got {llr_host.shape[1]}")
-    dec = HybridDecoder(code, bp_cfg, scl_cfg, capacity=B, chunk=bp_batch_size)
+    if decoder is None:
+        dec = HybridDecoder(code, bp_cfg, scl_cfg, capacity=B, chunk=bp_batch_size)
+    else:
+        dec = decoder
+        if dec.code is not code or dec.capacity < B or dec.chunk != bp_batch_size:
+            raise ValueError("decoder does not match the code, the batch size or the job count")
+        if bp_cfg is not None and replace(bp_cfg, stop_mode="crc") != dec.bp_cfg:
+            raise ValueError("decoder was built for another BP configuration")
+        if scl_cfg is not None and scl_cfg != dec.scl_cfg:
+            raise ValueError("decoder was built for another SCL configuration")
     pinned = torch.from_numpy(llr_host.astype(np.float32)).pin_memory()
     t_host0 = time.perf_counter()
     g0 = torch.zeros(1, dtype=torch.int64, device=dec.device)

@@ -223,11 +223,16 @@ def scl_decode_batch(
             raise ValueError("channel LLRs must be finite")
         x = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).cuda()
     else:
+        if llrs.dim() != 2 or llrs.shape[1] != code.N:
+            raise ValueError(f"expected llrs of shape (B, {code.N}), got {tuple(llrs.shape)}")
         x = llrs.to(torch.float32).contiguous()
     B = x.shape[0]
     dev = x.device
     NW = (code.N + 31) // 32
     MW = (code.message_len + 31) // 32
+    cur = torch.cuda.current_stream(dev)
+    if stream is not None:  # the launch stream sees the inputs and zeroed outputs made on the current stream
+        stream.wait_stream(cur)
     u = torch.zeros((B, NW), dtype=torch.int32, device=dev)
     mt = torch.zeros(B, dtype=torch.float32, device=dev)
     ok = torch.zeros(B, dtype=torch.uint8, device=dev)
@@ -238,6 +243,8 @@ def scl_decode_batch(
     ncfg = cfg.native()
     import ctypes
 
+    if stream is not None:
+        stream.wait_stream(cur)
     nat.check(
         lib.pc_scl_decode(
             nat.ptr(x), B, nat.ptr(queue), nat.ptr(count), dc.ref, ctypes.byref(ncfg), nat.ptr(u), nat.ptr(pw),
@@ -246,6 +253,11 @@ def scl_decode_batch(
         ),
         "pc_scl_decode",
     )
+    if stream is not None:  # results are read on the current stream; the temporaries outlive the launch
+        for t in (x, u, mt, ok, sel, pw, queue, count):
+            if t is not None:
+                t.record_stream(stream)
+        cur.wait_stream(stream)
     if not host:
         return SclBatchResult(u, mt, ok.bool(), sel.bool(), pw)
     return SclBatchResult(

@@ -40,3 +40,20 @@ def test_workload_lines(wl, frames):
         assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     if wl == "c1":
         assert d["fixed_cap"]["stop_mode"] == "none" and d["fixed_cap"]["frac"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("wl,frames", [("c4", 256), ("c3", 1024)])
+def test_gpus_flag_spawns_ranks_and_merges_counters(wl, frames):
+    """`bench.py --gpus 2` (no launcher) runs two ranks itself; on the one-GPU
+    box both share cuda:0 and merge over gloo.  The merged per-point counters
+    equal one rank decoding the same global frames (frames are keyed by their
+    global index, shard.shard_range)."""
+    common = ("--workload", wl, "--steps", "1", "--warmup", "3", "--no-cpu")
+    two = _line("--gpus", "2", "--frames", str(frames), *common)
+    one = _line("--frames", str(2 * frames), *common)
+    assert two["n_gpus"] == 2 and two["config"]["parallelism"] == "frame-sharded x2"
+    assert one["n_gpus"] == 1
+    keys = ("frames", "frame_errors", "bit_errors", "bp_iterations")
+    for a, b in zip(two["sweep"], one["sweep"]):
+        assert {k: a[k] for k in keys} == {k: b[k] for k in keys}

@@ -346,3 +346,48 @@ def test_persistent_kernel_matches_per_frame_ctas(N, mode):
         outs.append((u, su, it, cv))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("N,frames,ebno", [(1024, 2000, 2.0), (128, 1000, 2.0), (256, 500, 2.0), (4096, 200, 2.0)])
+def test_per_frame_api_equals_batch_api(N, frames, ebno):
+    """The reference's batch == per-frame contract (pkg/tests/test_hybrid.py:152-168):
+    bp_decode (per frame, soft outputs) and bp_decode_batch run the same kernel,
+    so u_hat, iterations, flags and soft values are bit-identical per frame, and
+    the hybrid's BP stage decides every frame the same way."""
+    import torch
+
+    from paper_1609_09358_b200 import HybridDecoder, SclConfig
+    from paper_1609_09358_b200 import _native as nat
+    from paper_1609_09358_b200.channel import make_frames
+
+    code = CodeConfig(N, N // 2, crc=16)
+    _, llrs = make_frames(code, ebno_to_sigma(ebno, code.rate), 91, 0, 0, frames)
+    llrs = llrs.astype(np.float32).astype(np.float64)
+    cfg = BpConfig(stop_mode="crc")
+    batch = bp_decode_batch(llrs, code, cfg, soft=True)
+    for f in range(frames):
+        one = bp_decode(llrs[f], code, cfg)
+        assert one.converged == batch.converged[f] and one.iterations_used == batch.iterations_used[f], f
+        assert np.array_equal(one.u_hat, batch.u_hat[f]), f
+        assert np.array_equal(one.soft_u, batch.soft_u[f]) and np.array_equal(one.soft_x, batch.soft_x[f]), f
+    dec = HybridDecoder(code, cfg, SclConfig(4), capacity=frames, chunk=256)
+    dec.run(torch.from_numpy(llrs.astype(np.float32)).cuda()).sync()
+    r = dec.host_results()
+    assert np.array_equal(r["converged"], batch.converged)
+    assert np.array_equal(r["iters"], batch.iterations_used)
+    pay = nat.unpack_bits(r["payload"], code.message_len)
+    cv = batch.converged
+    assert np.array_equal(pay[cv], batch.u_hat[cv][:, code.info_positions[: code.message_len]])
+
+
+@pytest.mark.parametrize("N", [128, 256, 1024, 2048])
+def test_soft_x_matches_oracle(N):
+    code = CodeConfig(N, N // 2, crc=16)
+    sigma = ebno_to_sigma(2.0, code.rate)
+    for f in range(4):
+        _, llr = make_frame(code, sigma, frame_rng(17, 1, f))
+        llr = llr.astype(np.float32).astype(np.float64)
+        res = bp_decode(llr, code, BpConfig(i_max=3, stop_mode="none"))
+        ref = oracle.bp_decode(llr, code, i_max=3, stop_mode="none")
+        assert mixed_err(res.soft_x, ref["soft_x"]) <= 1e-3
+        assert mixed_err(res.soft_u, ref["soft_u"]) <= 1e-3

@@ -100,3 +100,45 @@ def test_maximum_block_length_hybrid_chunks():
     agree = (bits == pay).all(axis=1)
     # frames may part only where BP provenance flips on a near-tie (test_gpu_hybrid.py)
     assert agree.mean() >= 0.95, np.flatnonzero(~agree)
+
+
+def test_tampered_first_info_is_refused_not_decoded():
+    """A reference-side binding that sets pc_code_t.first_info past info_pos[0]
+    gets PC_ERR_INVALID from pc_scl_decode (the struct's seal no longer
+    matches), not silently wrong decisions; pc_code_seal derives the right
+    value and rejects tables that contradict each other."""
+    import ctypes
+
+    import torch
+
+    from paper_1609_09358_b200 import _native as nat
+
+    code = CodeConfig(1024, 512, crc=16)
+    dc = nat.device_code(code)
+    assert dc.struct.first_info == int(code.info_positions[0]) == 191
+    lib = nat.load()
+    cfg = SclConfig(32).native()
+    llr = torch.ones((1, 1024), dtype=torch.float32, device="cuda")
+    u = torch.zeros((1, 32), dtype=torch.int32, device="cuda")
+    ws = dc.new_scl_workspace(cfg)
+    bad = nat.PcCode.from_buffer_copy(dc.struct)
+    bad.first_info = 224
+    rc = lib.pc_scl_decode(llr.data_ptr(), 1, None, None, ctypes.byref(bad), ctypes.byref(cfg), u.data_ptr(), None,
+                           None, None, None, None, ws.data_ptr(), nat.stream_handle())
+    assert rc == -1
+    # resealing derives first_info from the tables again
+    assert lib.pc_code_seal(ctypes.byref(bad), nat.stream_handle()) == 0 and bad.first_info == 191
+    assert lib.pc_scl_decode(llr.data_ptr(), 1, None, None, ctypes.byref(bad), ctypes.byref(cfg), u.data_ptr(),
+                             None, None, None, None, None, ws.data_ptr(), nat.stream_handle()) == 0
+    # info_pos that is not the ascending list of non-frozen positions is rejected
+    ip = dc.info_pos.clone()
+    ip[[0, 1]] = ip[[1, 0]]
+    wrong = nat.PcCode.from_buffer_copy(dc.struct)
+    wrong.info_pos = ip.data_ptr()
+    assert lib.pc_code_seal(ctypes.byref(wrong), nat.stream_handle()) == -1
+    fz = dc.frozen_bits.clone()
+    fz[0] ^= 1
+    wrong = nat.PcCode.from_buffer_copy(dc.struct)
+    wrong.frozen_bits = fz.data_ptr()
+    assert lib.pc_code_seal(ctypes.byref(wrong), nat.stream_handle()) == -1
+    torch.cuda.synchronize()

@@ -245,3 +245,18 @@ def test_scl_workspace_size_query_without_gpu():
     # v2 (N < 32) needs only the counter block
     assert lib.pc_scl_workspace_bytes(ctypes.byref(code_struct(16, 8, 0)), ctypes.byref(ps.SclConfig(4).native())) \
         == lib.pc_workspace_bytes()
+
+
+def test_c_abi_refuses_unsealed_code_without_gpu():
+    """A code struct that pc_code_seal never validated (or that changed after
+    sealing) is refused before any launch: first_info is derived by the
+    library, never trusted from the caller."""
+    lib = nat.load()
+    code = nat.PcCode(1024, 10, 512, 496, 16, 0, 0, 191, 16, 16, 16, 16, None)
+    cfg = nat.PcBpCfg(50, 0, 0, 0, 20.0)
+    assert lib.pc_bp_decode(16, 1, ctypes.byref(code), ctypes.byref(cfg), None, None, None, None, 16, 16,
+                            None, None) == -1
+    scfg = ps.SclConfig(32).native()
+    assert lib.pc_scl_decode(16, 1, None, None, ctypes.byref(code), ctypes.byref(scfg), None, None, None, None,
+                             None, None, 16, None) == -1
+    assert lib.pc_encode(16, 1, ctypes.byref(code), 16, None) == -1
