@@ -42,18 +42,72 @@ METRIC = "decoded info Gbit/s, hybrid BP+SCL N=1024 L=32, vs Eb/N0; p50 frame la
 EBNO = (1.0, 1.5, 2.0, 2.5, 3.0, 3.5, 4.0)
 N, K, LIST, IMAX = 1024, 512, 32, 50
 SEED = 20240917
-def mufu_per_alg_g(n: int, keep: bool) -> float:
+def mufu_per_alg_g(n: int) -> float:
     """MUFU ops K1 spends per ALGORITHMIC exact g (the reference's 2nN per
-    frame-iteration, bp.py:138-161).  A PE (two g) needs 3 exponentials and 4
-    logarithms (bp_math.cuh).  The R sweep evaluates its sum operand's
-    exponential on the FMA pipe (ex2_fma): 6 MUFU per R-sweep PE.  With kept
-    exponentials (N <= 2048) an L-sweep PE at boundaries 1..n-1 reuses the R
-    sweep's 2^-|a| (6 MUFU; 7 at boundary n); without them (N = 4096) the L
-    sweep also uses ex2_fma (6 MUFU everywhere).  R[n] (never read) is not
-    computed."""
-    r = (n - 1) * 6
-    l_ = 7 + (n - 1) * 6 if keep else 6 * n
-    return (r + l_) / 2 / (2 * n)  # per PE-pair of sweeps -> per g, over the 2n algorithmic g per node pair
+    frame-iteration, bp.py:138-161).  K1 runs the likelihood-ratio form
+    (bp_math.cuh, g_mode 0): one MUFU.RCP per g, and R[n] (never read) is not
+    computed, so a frame-iteration is (2n - 1) N/2 PEs x 2 RCP."""
+    return (2 * n - 1) / (2 * n)
+
+
+def k1_tpf(N: int) -> int:
+    """K1's default threads per frame for the likelihood-ratio form (bp2.cu
+    bp2_default_tpf: Q = 8 nodes per thread, at least one warp)."""
+    return max(32, N // 8)
+
+
+def _clock_mhz(ck):
+    peak_mhz = 1965.0
+    try:
+        peak_mhz = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("sm_max_mhz", 1965.0))
+    except Exception:
+        pass
+    return (ck or {}).get("sm_mhz") or peak_mhz, peak_mhz
+
+
+def k1_roofline(torch, dev, N: int, g_total: float, k1_s: float, ck, frames_per_launch=None) -> dict:
+    """Roofline of K1 from live numbers: g_total algorithmic exact-g
+    evaluations (sum of iterations x 2nN) in k1_s seconds of K1 time (CUDA
+    events on K1's stream).  K1 is bound by the SM instruction issue rate
+    (ncu: issue slots ~80% busy, XU ~67%, HBM < 1%), so `peak` is the issue
+    bound: 148 SM x 4 warp-instructions/clk at the measured SM clock divided by
+    the warp-instructions K1 executes per algorithmic g (one ncu capture of the
+    same kernel, profiles/k1_issue.json).  `frac_alg` is SURVEY.md section 8(d)'s
+    fixed formula (achieved x 4 MUFU per g / XU peak), which the
+    likelihood-ratio arithmetic exceeds by design (1 MUFU per g, not 4)."""
+    n = N.bit_length() - 1
+    achieved = g_total / k1_s / 1e9
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mhz, max_mhz = _clock_mhz(ck)
+    xu_ops = sms * 16 * mhz * 1e6
+    mpg = mufu_per_alg_g(n)
+    issue = None
+    try:
+        issue = json.loads((ROOT / "profiles" / "k1_issue.json").read_text())[str(N)]
+    except Exception:
+        pass
+    ipg = issue["warp_inst_per_alg_g"] if issue else None
+    peak = sms * 4 * mhz * 1e6 / ipg / 1e9 if ipg else None
+    traffic = None
+    try:
+        per_frame = json.loads((ROOT / "profiles" / "bp_kernel_ncu.json").read_text())["dram_bytes_per_frame"]
+        if N == 1024 and frames_per_launch:
+            traffic = per_frame * frames_per_launch
+    except Exception:
+        pass
+    return {
+        "bound": "issue", "achieved": achieved, "peak": peak, "unit": "Gg/s",
+        "frac": achieved / peak if peak else None, "traffic": traffic,
+        "frac_alg": achieved * 4 / (xu_ops / 1e9),
+        "kernel": f"k_bp2<{n},{k1_tpf(N)},0> (register/shuffle BP, likelihood-ratio arithmetic, "
+                  f"{k1_tpf(N)} threads/frame)",
+        "sm_mhz": mhz, "sm_max_mhz": max_mhz,
+        "warp_inst_per_alg_g": ipg, "issue_source": issue.get("source") if issue else None,
+        "xu": {"mufu_per_alg_g": mpg, "peak": xu_ops / mpg / 1e9, "frac": achieved * mpg / (xu_ops / 1e9)},
+        "note": "unit = one exact-g evaluation as the reference counts them (2nN per frame-iteration, "
+                "bp.py:138-161); frac = share of the SM issue bound; frac_alg = SURVEY 8(d)'s XU formula at 4 "
+                "MUFU per g; xu = the MUFU pipe at K1's 1 RCP per g; HBM < 1% (4.2 KB per frame)",
+    }
 
 
 WORKLOAD = "hybrid BP->SCL N=1024 K=512 (496 payload + CRC-16) L=32 i_max=50, Eb/N0 1-4 dB step 0.5"
@@ -233,6 +287,7 @@ def run_gpu(args):
 
     # ---- timed region (device time, events on the launching streams) ----
     dec.kernel_events = []
+    dec.scl_events = []
     lat_p50, gammas, iters_sum, pt_ms = [[] for _ in EBNO], [[] for _ in EBNO], [0] * len(EBNO), [0.0] * len(EBNO)
     with ClockSampler(local) as clocks:
         barrier()
@@ -249,7 +304,9 @@ def run_gpu(args):
     elapsed_ms = t_start.elapsed_time(t_end)
     # per-point times and BP kernel times
     bp_ms = [a.elapsed_time(b) for a, b in dec.kernel_events]
+    scl_ms = [a.elapsed_time(b) for a, b in (dec.scl_events or [])]
     dec.kernel_events = None
+    dec.scl_events = None
     for step_rec, _ in records:
         for p, (a, b) in enumerate(step_rec):
             pt_ms[p] += a.elapsed_time(b)
@@ -288,37 +345,19 @@ def run_gpu(args):
     n = code.n
     g_per_step = sum(local_iters) * 2 * n * N  # iterations are deterministic per input set
     bp_ms_step = sum(bp_ms) / args.steps
-    achieved = g_per_step / (bp_ms_step * 1e-3) / 1e9  # Gg/s
     ck = clocks.summary()
-    peak_mhz = 1965.0
-    try:
-        peak_mhz = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("sm_max_mhz", 1965.0))
-    except Exception:
-        pass
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    mpg = mufu_per_alg_g(code.n, True)
-    peak = sms * 16 * peak_mhz * 1e6 / mpg / 1e9  # MUFU ops/s / MUFU per algorithmic exact g, in Gg/s
-    traffic = None
-    prof = ROOT / "profiles" / "bp_kernel_ncu.json"
-    if prof.exists():
-        try:
-            # measured DRAM bytes per frame (one ncu --set full capture) x this launch's frames
-            traffic = json.loads(prof.read_text())["dram_bytes_per_frame"] * dec.chunk
-        except Exception:
-            traffic = None
-    roofline = {
-        "bound": "xu", "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
-        "traffic": traffic, "kernel": "k_bp2<10,256,0> (register/shuffle BP, TPF=256)",
-        "traffic_source": "profiles/bp_kernel_ncu.json: dram__bytes_read+write per frame x frames per launch",
-        "note": "exact-g node updates/s of K1 vs the MUFU (XU) pipe bound: 148 SM x 16 MUFU/clk x sm_max_mhz / "
-                "MUFU per algorithmic g (2nN per frame-iteration, the reference's count; 7 MUFU per PE, 6 in the "
-                "L sweep with kept exponentials, R[n] not computed); HBM is <1% (4.2 KB/frame)",
-        "peak_at_measured_clock": (sms * 16 * ck["sm_mhz"] * 1e6 / mpg / 1e9) if ck.get("sm_mhz") else None,
-        "mufu_per_algorithmic_g": mpg,
-        # K1's own HBM traffic: read the LLRs, write payload + iters + flag + stamp per frame
-        "hbm_gbs": len(EBNO) * B * (4 * N + 4 * MW + 4 + 1 + 8) / (bp_ms_step * 1e-3) / 1e9,
-        "bp_share_of_step": bp_ms_step / (max_ms / args.steps),
-    }
+    roofline = k1_roofline(torch, dev, N, g_per_step, bp_ms_step * 1e-3, ck, dec.chunk)
+    roofline["traffic_source"] = "profiles/bp_kernel_ncu.json: dram__bytes_read+write per frame x frames per launch"
+    # K1's own HBM traffic: read the LLRs, write payload + iters + flag + stamp per frame
+    roofline["hbm_gbs"] = len(EBNO) * B * (4 * N + 4 * MW + 4 + 1 + 8) / (bp_ms_step * 1e-3) / 1e9
+    roofline["bp_share_of_step"] = bp_ms_step / (max_ms / args.steps)
+    # K3 (SCL on the BP failures): frames/s and share of the step
+    scl_ms_step = sum(scl_ms) / args.steps if scl_ms else None
+    k3 = None
+    if scl_ms_step:
+        nscl = sum(round(gammas[p] * B * world) for p in range(len(EBNO))) / world
+        k3 = {"kernel": f"k_scl3<{LIST}> (CRC-aided SCL, one warp per frame)", "frames_per_step": nscl,
+              "mframes_per_s": nscl / (scl_ms_step * 1e-3) / 1e6, "share_of_step": scl_ms_step / (max_ms / args.steps)}
 
     # ---- e2e: the public host-buffer call, H2D + decode + D2H inside the timed region ----
     e2e_val = None
@@ -370,6 +409,7 @@ def run_gpu(args):
             "p50_latency_ms": float(np.median([s["p50_latency_ms"] for s in sweep])),
             "sweep": sweep,
             "roofline": roofline,
+            "k3": k3,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "Gbit/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": args.steps * len(EBNO) * ((B + dec.chunk - 1) // dec.chunk) * dec.launches_per_chunk,
@@ -419,16 +459,6 @@ def _cpu_sample(sample, fpp, fixed, min_s=2.0, cap=1 << 16):
         fpp = min(cap, fpp * 4)
         busy, bits = sample(fpp)
     return fpp, busy, bits
-
-
-def _xu_peak_gg(torch, dev, mpg):
-    peak_mhz = 1965.0
-    try:
-        peak_mhz = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("sm_max_mhz", 1965.0))
-    except Exception:
-        pass
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    return sms * 16 * peak_mhz * 1e6 / mpg / 1e9
 
 
 BP_WORKLOADS = {
@@ -522,9 +552,6 @@ def run_bp_workload(args):
     max_ms = max_over_ranks(ms, device=COMM)
     value = world * B * m * len(pts) * args.steps / (max_ms * 1e-3) / 1e9
     g_step = int(it_sum.sum()) * 2 * code.n * n4
-    achieved = g_step / (sum(pt_ms) * 1e-3) / 1e9
-    # N <= 2048 keeps the R sweep's exponentials; N = 4096 does not (FMA exp2 in both sweeps)
-    peak = _xu_peak_gg(torch, dev, mufu_per_alg_g(code.n, code.n <= 11))
     # e2e: pinned host LLRs -> device, decode, payload + flags -> host, every step
     host = [torch.empty((B, n4), dtype=torch.float32, pin_memory=True) for _ in pts]
     for p in range(len(pts)):
@@ -593,15 +620,18 @@ def run_bp_workload(args):
         barrier()
         fms = max_over_ranks(a.elapsed_time(b) / args.steps, device=COMM)
         fg = B * IMAX * 2 * code.n * n4 / (fms * 1e-3) / 1e9
+        rf = k1_roofline(torch, dev, n4, B * IMAX * 2 * code.n * n4, fms * 1e-3, None)
         fixed = {"stop_mode": "none", "i_max": IMAX, "ms_per_batch": fms,
                  "frame_iterations_per_s": world * B * IMAX / (fms * 1e-3),
-                 "gbps": world * B * m / (fms * 1e-3) / 1e9, "achieved_gg_s": fg, "frac": fg / peak}
+                 "gbps": world * B * m / (fms * 1e-3) / 1e9, "achieved_gg_s": fg, "frac": rf["frac"],
+                 "frac_alg": rf["frac_alg"]}
     e2e_run(1)
     barrier()
     te = time.perf_counter()
     e2e_run(args.steps)
     barrier()
     e2e_val = world * B * m * len(pts) * args.steps / max_over_ranks(time.perf_counter() - te, device=COMM) / 1e9
+    roofline = k1_roofline(torch, dev, n4, g_step, sum(pt_ms) * 1e-3, clocks.summary())
     if rank == 0:
         cpu = None
         if not args.no_cpu:
@@ -639,11 +669,7 @@ def run_bp_workload(args):
                        "bp_iterations": int(stats[p, 0]), "bit_errors": int(stats[p, 1]),
                        "frame_errors": int(stats[p, 2]), "bp_failures": int(stats[p, 3])}
                       for p, eb in enumerate(pts)],
-            "roofline": {"bound": "xu", "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": wl["kernel"],
-                         "note": "exact-g node updates/s (2nN per frame-iteration) vs 148 SM x 16 MUFU/clk / "
-                                 f"{mufu_per_alg_g(code.n, code.n <= 11):.3f} MUFU per algorithmic g "
-                                 "(bench.mufu_per_alg_g; R[n] not computed)"},
+            "roofline": roofline,
             "fixed_cap": fixed,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "Gbit/s", "h2d_bytes_per_step": B * n4 * 4 * len(pts),

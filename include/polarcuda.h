@@ -75,8 +75,11 @@ typedef struct pc_code {
  * Mirrors the validation of CodeConfig.__init__ (polar.py:235-263). */
 int pc_code_seal(pc_code_t *code, void *stream);
 
-/* BpConfig, bp.py:40-57.  g_mode 0 = exact, 1 = min, 2 = exact evaluated per g
- * (4 MUFU, the pre-exponential-domain form; N = 1024/2048, parity studies); stop_mode 0 = crc,
+/* BpConfig, bp.py:40-57.  g_mode 0 = exact (likelihood-ratio arithmetic:
+ * messages e^v, g = (1 + xy)/(x + y), one reciprocal per g), 1 = min, 2 = exact
+ * evaluated per g (4 MUFU, natural log domain; N = 1024/2048, parity studies),
+ * 3 = exact in the round-1 exponential/log2 form (2.875 MUFU per g; register/
+ * shuffle kernel only, N = 128..4096; an A/B knob); stop_mode 0 = crc,
  * 1 = reencode, 2 = none.  threads_per_frame 0 = library default.
  * kernel: 0 = auto (register/shuffle kernel when eligible), 1 = shared-memory
  * kernel, 2 = register/shuffle kernel (N = 128..4096, every stop rule, the

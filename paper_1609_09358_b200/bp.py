@@ -68,7 +68,7 @@ class BpConfig:
     def native(self, threads_per_frame: int = 0, kernel: int | None = None) -> nat.PcBpCfg:
         return nat.PcBpCfg(
             self.i_max,
-            _G_MODES.index(self.g_mode),
+            _G_MODES.index(self.g_mode) or (3 if nat.env_int("PC_BP_LOGDOMAIN", 0) else 0),
             _STOP_MODES.index(self.stop_mode),
             threads_per_frame or nat.env_int("PC_BP_TPF", 0),
             float(self.llr_max),

@@ -132,7 +132,7 @@ int pc_bp_decode(const float *llr, int32_t B, const pc_code_t *code, const pc_bp
         return rc;
     if (cfg == nullptr || B < 0 || (B > 0 && (llr == nullptr || iters == nullptr || converged == nullptr)))
         return PC_ERR_INVALID;
-    if (cfg->i_max < 1 || cfg->g_mode < 0 || cfg->g_mode > 2 || cfg->stop_mode < 0 || cfg->stop_mode > 2 ||
+    if (cfg->i_max < 1 || cfg->g_mode < 0 || cfg->g_mode > 3 || cfg->stop_mode < 0 || cfg->stop_mode > 2 ||
         cfg->kernel < 0 || cfg->kernel > 2 || !(cfg->llr_max > 0.0f))
         return PC_ERR_INVALID;
     if (cfg->stop_mode == 0 && (code->crc_width == 0 || code->crc_cols == nullptr))
@@ -162,7 +162,7 @@ int pc_bp_iterate(float *l_msgs, float *r_msgs, int32_t B, const pc_code_t *code
     if (rc)
         return rc;
     if (cfg == nullptr || B < 0 || (B > 0 && (l_msgs == nullptr || r_msgs == nullptr)) || cfg->g_mode < 0 ||
-        cfg->g_mode > 1 || !(cfg->llr_max > 0.0f))
+        cfg->g_mode > 3 || cfg->g_mode == 2 || !(cfg->llr_max > 0.0f))
         return PC_ERR_INVALID;
     return launch_bp_iterate(l_msgs, r_msgs, B, code->n, cfg->g_mode, cfg->llr_max, (cudaStream_t)stream);
 }

@@ -30,23 +30,23 @@ namespace pc {
 // Rprev = R[j-1] (nullptr for j == 1: use the frozen prior), Lj = L[j].
 template <int GMODE, bool RSWEEP>
 __device__ __forceinline__ void bp_pe(int j, int p, const float *__restrict__ Rprev, const float *__restrict__ Lj,
-                                      const uint32_t *frz, float lim, float &o1, float &o2, float &av, float &r2)
+                                      const uint32_t *frz, BpLim lim, float &o1, float &o2, float &av, float &r2)
 {
     const int h = 1 << (j - 1);
     const int i1 = ((p >> (j - 1)) << j) | (p & (h - 1));
     const int i2 = i1 + h;
     if (Rprev == nullptr) {
-        av = bit_of(frz, i1) ? lim : 0.0f;
-        r2 = bit_of(frz, i2) ? lim : 0.0f;
+        av = bit_of(frz, i1) ? bp_prior<GMODE>(lim) : bp_zero<GMODE>();
+        r2 = bit_of(frz, i2) ? bp_prior<GMODE>(lim) : bp_zero<GMODE>();
     } else {
         av = Rprev[i1];
         r2 = Rprev[i2];
     }
     const float l1 = Lj[i1], l2 = Lj[i2];
     if (RSWEEP)
-        bp_pe2<GMODE, true>(av, l2 + r2, l1, r2, lim, o1, o2);
+        bp_pe2<GMODE, true>(av, bp_comb<GMODE>(l2, r2), l1, r2, lim, o1, o2);
     else
-        bp_pe2<GMODE, false>(l1, l2 + r2, av, l2, lim, o1, o2);
+        bp_pe2<GMODE, false>(l1, bp_comb<GMODE>(l2, r2), av, l2, lim, o1, o2);
 }
 
 template <int LOGN>
@@ -79,18 +79,17 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int f = blockIdx.x;
-    constexpr float KIN = bp_unit_in<GMODE>(), KOUT = bp_unit_out<GMODE>();
-    const float lim = a.llr_max * KIN; // messages in the kernel's units (bp_math.cuh)
+    const BpLim lim = bp_lim<GMODE>(a.llr_max); // clip bounds in the mode's message domain (bp_math.cuh)
 
     for (int w = tid; w < NW; w += TPF)
         frz[w] = a.code.frozen_bits[w];
     const float *x = a.llr + (size_t)f * N;
     float *Lch = Ls + (LOGN - 1) * N;
     for (int i = tid; i < N; i += TPF)
-        Lch[i] = clampf(__ldg(x + i) * KIN, lim);
+        Lch[i] = bp_load<GMODE>(__ldg(x + i), a.llr_max);
     for (int i = tid; i < (LOGN - 1) * N; i += TPF) {
-        Rs[i] = 0.0f;
-        Ls[i] = 0.0f;
+        Rs[i] = bp_zero<GMODE>();
+        Ls[i] = bp_zero<GMODE>();
     }
     // CRC columns of the two nodes each boundary-1 element decides.
     uint32_t col[PPT][2];
@@ -143,8 +142,8 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
                     Ls[(j - 2) * N + i1] = o1;
                     Ls[(j - 2) * N + i2] = o2;
                 } else {
-                    su[q][0] = o1 + av; // soft_u = L[0] + R[0] on nodes 2p, 2p+1
-                    su[q][1] = o2 + r2;
+                    su[q][0] = bp_comb<GMODE>(o1, av); // soft_u = L[0] + R[0] on nodes 2p, 2p+1
+                    su[q][1] = bp_comb<GMODE>(o2, r2);
                 }
             }
             if (j > 1)
@@ -155,8 +154,8 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
             uint32_t syn = 0;
 #pragma unroll
             for (int q = 0; q < PPT; ++q) {
-                syn ^= (su[q][0] < 0.0f) ? col[q][0] : 0u;
-                syn ^= (su[q][1] < 0.0f) ? col[q][1] : 0u;
+                syn ^= bp_neg<GMODE>(su[q][0]) ? col[q][0] : 0u;
+                syn ^= bp_neg<GMODE>(su[q][1]) ? col[q][1] : 0u;
             }
             syn = __reduce_xor_sync(FULL, syn);
             if (lane == 0)
@@ -171,8 +170,8 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
 #pragma unroll
             for (int q = 0; q < PPT; ++q) {
                 const int p = tid + q * TPF;
-                ub[2 * p] = su[q][0] < 0.0f;
-                ub[2 * p + 1] = su[q][1] < 0.0f;
+                ub[2 * p] = bp_neg<GMODE>(su[q][0]);
+                ub[2 * p + 1] = bp_neg<GMODE>(su[q][1]);
             }
             __syncthreads();
             for (int h = 1; h < N; h <<= 1) { // polar_transform on the byte vector
@@ -184,7 +183,7 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
             }
             int bad = 0;
             for (int i = tid; i < N; i += TPF)
-                bad |= ub[i] != (uint8_t)((Lch[i] + Rn[i]) < 0.0f);
+                bad |= ub[i] != (uint8_t)bp_neg<GMODE>(bp_comb<GMODE>(Lch[i], Rn[i]));
             stop = !__syncthreads_or(bad);
         } else {
             __syncthreads();
@@ -205,9 +204,9 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
         const int p = tid + q * TPF;
         if (a.soft_u != nullptr)
             *reinterpret_cast<float2 *>(a.soft_u + (size_t)f * N + 2 * p) =
-                make_float2(su[q][0] * KOUT, su[q][1] * KOUT);
-        ub[2 * p] = su[q][0] < 0.0f;
-        ub[2 * p + 1] = su[q][1] < 0.0f;
+                make_float2(bp_store<GMODE>(su[q][0]), bp_store<GMODE>(su[q][1]));
+        ub[2 * p] = bp_neg<GMODE>(su[q][0]);
+        ub[2 * p + 1] = bp_neg<GMODE>(su[q][1]);
     }
     if (a.soft_x != nullptr) {
         // R[n] from the final R[n-1] and L[n] (R[n] is not read by the sweeps).
@@ -217,8 +216,8 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
             bp_pe<GMODE, true>(LOGN, p, Rp, Lch, frz, lim, o1, o2, av, r2);
             int i1, i2;
             pe_nodes<LOGN>(LOGN, p, i1, i2);
-            a.soft_x[(size_t)f * N + i1] = (Lch[i1] + o1) * KOUT;
-            a.soft_x[(size_t)f * N + i2] = (Lch[i2] + o2) * KOUT;
+            a.soft_x[(size_t)f * N + i1] = bp_store<GMODE>(bp_comb<GMODE>(Lch[i1], o1));
+            a.soft_x[(size_t)f * N + i2] = bp_store<GMODE>(bp_comb<GMODE>(Lch[i2], o2));
         }
     }
     __syncthreads();
@@ -244,19 +243,20 @@ __global__ void __launch_bounds__(TPF) k_bp_decode(const BpArgs a)
 // SMEM = true stages the frame's state in shared memory (N <= 2048); for
 // N = 4096 (426 KB of state) the same sweeps run in place on global memory.
 template <int GMODE, bool SMEM>
-__global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float lim)
+__global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float llr_max)
 {
     extern __shared__ __align__(16) float st[];
     const int N = 1 << n;
     const size_t base = (size_t)blockIdx.x * (n + 1) * N;
-    constexpr float KIN = bp_unit_in<GMODE>(), KOUT = bp_unit_out<GMODE>();
+    constexpr float KIN = bp_unit_in<GMODE>();
     float *L = SMEM ? st : l_msgs + base;
     float *R = SMEM ? st + (size_t)(n + 1) * N : r_msgs + base;
-    const float lim_out = lim;
-    lim *= KIN;
-    for (int i = threadIdx.x; i < (n + 1) * N; i += blockDim.x) { // into the kernel's message units
-        L[i] = l_msgs[base + i] * KIN;
-        R[i] = r_msgs[base + i] * KIN;
+    const float lim_out = llr_max;
+    const BpLim lim = bp_lim<GMODE>(llr_max);
+    for (int i = threadIdx.x; i < (n + 1) * N; i += blockDim.x) { // into the mode's message domain
+        const float l = l_msgs[base + i] * KIN, r = r_msgs[base + i] * KIN;
+        L[i] = GMODE == 0 ? ex2_approx(l) : l;
+        R[i] = GMODE == 0 ? ex2_approx(r) : r;
     }
     __syncthreads();
     const int NPE = N / 2;
@@ -267,7 +267,7 @@ __global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float lim)
             const float av = R[(j - 1) * N + i1], r2 = R[(j - 1) * N + i2];
             const float l1 = L[j * N + i1], l2 = L[j * N + i2];
             float o1, o2;
-            bp_pe2<GMODE, true>(av, l2 + r2, l1, r2, lim, o1, o2);
+            bp_pe2<GMODE, true>(av, bp_comb<GMODE>(l2, r2), l1, r2, lim, o1, o2);
             R[j * N + i1] = o1;
             R[j * N + i2] = o2;
         }
@@ -280,15 +280,15 @@ __global__ void k_bp_iterate(float *l_msgs, float *r_msgs, int n, float lim)
             const float av = R[(j - 1) * N + i1], r2 = R[(j - 1) * N + i2];
             const float l1 = L[j * N + i1], l2 = L[j * N + i2];
             float o1, o2;
-            bp_pe2<GMODE, false>(l1, l2 + r2, av, l2, lim, o1, o2);
+            bp_pe2<GMODE, false>(l1, bp_comb<GMODE>(l2, r2), av, l2, lim, o1, o2);
             L[(j - 1) * N + i1] = o1;
             L[(j - 1) * N + i2] = o2;
         }
         __syncthreads();
     }
     for (int i = threadIdx.x; i < (n + 1) * N; i += blockDim.x) {
-        l_msgs[base + i] = clampf(L[i] * KOUT, lim_out);
-        r_msgs[base + i] = clampf(R[i] * KOUT, lim_out);
+        l_msgs[base + i] = clampf(bp_store<GMODE>(L[i]), lim_out);
+        r_msgs[base + i] = clampf(bp_store<GMODE>(R[i]), lim_out);
     }
 }
 
@@ -357,11 +357,11 @@ int launch_bp_decode(const BpArgs &a, int g_mode, int tpf, int kernel, cudaStrea
 {
     if (a.B == 0)
         return PC_OK;
-    if (g_mode == 2)
+    if (g_mode == 2 || g_mode == 3) // exact g, per-g / round-1 log-domain forms: K1 v2 only
         return launch_bp2(a, g_mode, tpf, s);
-    if (kernel == 2 && !bp2_eligible(a, tpf))
+    if (kernel == 2 && !bp2_eligible(a, g_mode, tpf))
         return PC_ERR_UNSUPPORTED;
-    if (kernel != 1 && bp2_eligible(a, tpf))
+    if (kernel != 1 && bp2_eligible(a, g_mode, tpf))
         return launch_bp2(a, g_mode, tpf, s);
     return g_mode == 0 ? launch_bp_g<0>(a, a.code.n, tpf, s) : launch_bp_g<1>(a, a.code.n, tpf, s);
 }
@@ -373,11 +373,11 @@ int launch_bp_iterate(float *l, float *r, int B, int n, int g_mode, float lim, c
     const size_t smem = (size_t)2 * (n + 1) * ((size_t)1 << n) * sizeof(float);
     const int threads = (1 << (n - 1)) >= 256 ? 256 : (1 << (n - 1));
     if (smem > 200 * 1024) {
-        auto kern = g_mode == 0 ? k_bp_iterate<0, false> : k_bp_iterate<1, false>;
+        auto kern = g_mode == 0 ? k_bp_iterate<0, false> : (g_mode == 1 ? k_bp_iterate<1, false> : k_bp_iterate<3, false>);
         kern<<<B, threads, 0, s>>>(l, r, n, lim);
         return cudaGetLastError() == cudaSuccess ? PC_OK : PC_ERR_CUDA;
     }
-    auto kern = g_mode == 0 ? k_bp_iterate<0, true> : k_bp_iterate<1, true>;
+    auto kern = g_mode == 0 ? k_bp_iterate<0, true> : (g_mode == 1 ? k_bp_iterate<1, true> : k_bp_iterate<3, true>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return PC_ERR_CUDA;
     kern<<<B, threads, smem, s>>>(l, r, n, lim);

@@ -34,7 +34,7 @@ struct ilog2<1> {
     static constexpr int value = 0;
 };
 
-// Exponential reuse (GMODE 0): the R sweep's 2^-|a| of every PE at boundaries
+// Exponential reuse (GMODE 3, the log-domain form): the R sweep's 2^-|a| of every PE at boundaries
 // 2..n-1 is kept in shared memory (one float per PE) and reused by the L sweep,
 // where a is the PE's second operand: 6 MUFU instead of 7 for those PEs.
 __host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
@@ -49,7 +49,7 @@ __host__ __device__ constexpr int bp2_base_bytes(int logn, int tpf)
 // tools/bp_tpf_probe.py.)  The KEPT(j) logic supports any prefix count.
 __host__ __device__ constexpr int bp2_keep(int logn, int tpf, int gmode)
 {
-    return gmode == 0 && bp2_base_bytes(logn, tpf) + (logn - 2) * (1 << logn) * 2 <= 225 * 1024 ? logn - 2 : 0;
+    return gmode == 3 && bp2_base_bytes(logn, tpf) + (logn - 2) * (1 << logn) * 2 <= 225 * 1024 ? logn - 2 : 0;
 }
 __host__ __device__ constexpr int bp2_keep_bytes(int logn, int tpf, int gmode)
 {
@@ -83,8 +83,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int f = blockIdx.x;
-    constexpr float KIN = bp_unit_in<GMODE>(), KOUT = bp_unit_out<GMODE>();
-    const float lim = a.llr_max * KIN; // messages in the kernel's units (bp_math.cuh)
+    const BpLim lim = bp_lim<GMODE>(a.llr_max); // clip bounds in the mode's message domain (bp_math.cuh)
     const int base = warp * 32 * Q + lane * Q;
 
     // the frame's channel LLRs land in L[n] by a TMA bulk copy while the
@@ -110,20 +109,20 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
         tma_load_1d(Lch, a.llr + (size_t)f * N, N * sizeof(float), &ch_bar);
     // (the R rows are written by the R sweep before any read; only L starts at 0)
     for (int i = tid; i < (NSL - 1) * N; i += TPF)
-        Ls[i] = 0.0f;
+        Ls[i] = bp_zero<GMODE>();
     mbar_wait(&ch_bar, phase);
     phase ^= 1u;
     for (int i = 4 * tid; i < N; i += 4 * TPF) {
         const float4 v = *reinterpret_cast<const float4 *>(Lch + i);
-        *reinterpret_cast<float4 *>(Lch + i) = make_float4(clampf(v.x * KIN, lim), clampf(v.y * KIN, lim),
-                                                          clampf(v.z * KIN, lim), clampf(v.w * KIN, lim));
+        *reinterpret_cast<float4 *>(Lch + i) = make_float4(bp_load<GMODE>(v.x, a.llr_max), bp_load<GMODE>(v.y, a.llr_max),
+                                                          bp_load<GMODE>(v.z, a.llr_max), bp_load<GMODE>(v.w, a.llr_max));
     }
     float Rr[NREG][Q], Lr[NREG][Q];
 #pragma unroll
     for (int s = 0; s < NREG; ++s)
 #pragma unroll
         for (int r = 0; r < Q; ++r)
-            Rr[s][r] = Lr[s][r] = 0.0f;
+            Rr[s][r] = Lr[s][r] = bp_zero<GMODE>();
     uint32_t col[Q];
 #pragma unroll
     for (int r = 0; r < Q; ++r)
@@ -133,14 +132,14 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
     float pri[Q];
 #pragma unroll
     for (int r = 0; r < Q; ++r)
-        pri[r] = ((fw >> r) & 1u) ? lim : 0.0f;
+        pri[r] = ((fw >> r) & 1u) ? bp_prior<GMODE>(lim) : bp_zero<GMODE>();
 
     // compile-time stage accessors (every loop below is fully unrolled, so the
     // register arrays are indexed with constants)
 #define KEPT(j) ((j) >= 2 && (j) - 2 < KEEP)
 #define PA(j, k) Pa[(((j) - 2) * (Q / 2) + (k)) * TPF + tid]
 #define PAP(j, p) Pa[((j) - 2) * (N / 2) + (p)] // shared-memory boundaries: indexed by PE
-    const float pprior = GMODE == 0 ? ex2_approx(-lim) : 0.0f; // 2^-|R[0]| of a frozen node
+    const float pprior = GMODE == 3 ? ex2_approx(-lim.hi) : 0.0f; // 2^-|R[0]| of a frozen node
 #define RGET(s, r) ((s) == 0 ? pri[r] : ((s) <= NREG ? Rr[(s) > 0 ? (s) - 1 : 0][r] : Rs[((s) - BW) * N + base + (r)]))
 #define LGET(s, r) ((s) <= NREG ? Lr[(s) > 0 ? (s) - 1 : 0][r] : Ls[((s) - BW) * N + base + (r)])
 
@@ -161,10 +160,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 const float av = RGET(j - 1, r1), r2v = RGET(j - 1, r2), l1 = LGET(j, r1), l2 = LGET(j, r2);
                 if (KEPT(j)) {
                     float px;
-                    bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, Rr[j - 1][r1], Rr[j - 1][r2], px);
+                    bp_pe2_keep(av, bp_comb<GMODE>(l2, r2v), l1, r2v, lim, Rr[j - 1][r1], Rr[j - 1][r2], px);
                     PA(j, ((r1 >> j) << (j - 1)) | (r1 & (h - 1))) = px;
                 } else {
-                    bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, Rr[j - 1][r1], Rr[j - 1][r2]);
+                    bp_pe2<GMODE, true>(av, bp_comb<GMODE>(l2, r2v), l1, r2v, lim, Rr[j - 1][r1], Rr[j - 1][r2]);
                 }
             }
         }
@@ -191,10 +190,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 float o1, o2;
                 if (KEPT(j)) {
                     float px;
-                    bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, o1, o2, px);
+                    bp_pe2_keep(av, bp_comb<GMODE>(l2, r2v), l1, r2v, lim, o1, o2, px);
                     PA(j, k) = px;
                 } else {
-                    bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                    bp_pe2<GMODE, true>(av, bp_comb<GMODE>(l2, r2v), l1, r2v, lim, o1, o2);
                 }
                 const float back = __shfl_xor_sync(0xffffffffu, hi ? o1 : o2, msk); // my output the partner computed
                 Rn[k] = hi ? back : o1;
@@ -233,10 +232,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                         const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
                         if (KEPT(j)) {
                             float px;
-                            bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, o[2 * e], o[2 * e + 1], px);
+                            bp_pe2_keep(av, bp_comb<GMODE>(l2, r2v), l1, r2v, lim, o[2 * e], o[2 * e + 1], px);
                             PAP(j, ((i1 >> j) << (j - 1)) | (i1 & (h - 1))) = px;
                         } else {
-                            bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, o[2 * e], o[2 * e + 1]);
+                            bp_pe2<GMODE, true>(av, bp_comb<GMODE>(l2, r2v), l1, r2v, lim, o[2 * e], o[2 * e + 1]);
                         }
                     }
                     Rd[n0] = o[0];
@@ -250,10 +249,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                         float p1, p2;
                         if (KEPT(j + 1)) {
                             float px;
-                            bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, p1, p2, px);
+                            bp_pe2_keep(av, bp_comb<GMODE>(l2, r2v), l1, r2v, lim, p1, p2, px);
                             PAP(j + 1, ((i1 >> (j + 1)) << j) | (i1 & (2 * h - 1))) = px;
                         } else {
-                            bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, p1, p2);
+                            bp_pe2<GMODE, true>(av, bp_comb<GMODE>(l2, r2v), l1, r2v, lim, p1, p2);
                         }
                         Rd2[i1] = p1;
                         Rd2[i2] = p2;
@@ -268,10 +267,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                     float o1, o2;
                     if (KEPT(j)) {
                         float px;
-                        bp_pe2_keep(av, l2 + r2v, l1, r2v, lim, o1, o2, px);
+                        bp_pe2_keep(av, bp_comb<GMODE>(l2, r2v), l1, r2v, lim, o1, o2, px);
                         PAP(j, p) = px;
                     } else {
-                        bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                        bp_pe2<GMODE, true>(av, bp_comb<GMODE>(l2, r2v), l1, r2v, lim, o1, o2);
                     }
                     Rd[i1] = o1;
                     Rd[i2] = o2;
@@ -303,10 +302,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                         const float av = Rj[i1], r2v = Rj[i2], l1 = Lt[i1], l2 = Lt[i2];
                         float o1, o2;
                         if (KEPT(j + 1))
-                            bp_pe2_p2(l1, l2 + r2v, av, PAP(j + 1, ((i1 >> (j + 1)) << j) | (i1 & (2 * h - 1))), l2,
+                            bp_pe2_p2(l1, bp_comb<GMODE>(l2, r2v), av, PAP(j + 1, ((i1 >> (j + 1)) << j) | (i1 & (2 * h - 1))), l2,
                                       lim, o1, o2);
                         else
-                            bp_pe2<GMODE, false, KEEP == 0 && GMODE == 0>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                            bp_pe2<GMODE, false, KEEP == 0 && GMODE == 3>(l1, bp_comb<GMODE>(l2, r2v), av, l2, lim, o1, o2);
                         m[e] = o1;
                         m[e + 2] = o2;
                     }
@@ -320,10 +319,10 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                         const float av = Rp[i1], r2v = Rp[i2], l1 = m[2 * e], l2 = m[2 * e + 1];
                         float o1, o2;
                         if (KEPT(j))
-                            bp_pe2_p2(l1, l2 + r2v, av, PAP(j, ((i1 >> j) << (j - 1)) | (i1 & (h - 1))), l2, lim, o1,
+                            bp_pe2_p2(l1, bp_comb<GMODE>(l2, r2v), av, PAP(j, ((i1 >> j) << (j - 1)) | (i1 & (h - 1))), l2, lim, o1,
                                       o2);
                         else
-                            bp_pe2<GMODE, false, KEEP == 0 && GMODE == 0>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                            bp_pe2<GMODE, false, KEEP == 0 && GMODE == 3>(l1, bp_comb<GMODE>(l2, r2v), av, l2, lim, o1, o2);
                         Ld[i1] = o1;
                         Ld[i2] = o2;
                     }
@@ -341,9 +340,9 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                     const float av = Rp[i1], r2v = Rp[i2], l1 = Lj[i1], l2 = Lj[i2];
                     float o1, o2;
                     if (KEPT(j))
-                        bp_pe2_p2(l1, l2 + r2v, av, PAP(j, p), l2, lim, o1, o2);
+                        bp_pe2_p2(l1, bp_comb<GMODE>(l2, r2v), av, PAP(j, p), l2, lim, o1, o2);
                     else
-                        bp_pe2<GMODE, false, KEEP == 0 && GMODE == 0>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                        bp_pe2<GMODE, false, KEEP == 0 && GMODE == 3>(l1, bp_comb<GMODE>(l2, r2v), av, l2, lim, o1, o2);
                     Ld[i1] = o1;
                     Ld[i2] = o2;
                 }
@@ -367,9 +366,9 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 const float av = hi ? pr : myR, r2v = hi ? myR : pr, l1 = hi ? pl : myL, l2 = hi ? myL : pl;
                 float o1, o2;
                 if (KEPT(j))
-                    bp_pe2_p2(l1, l2 + r2v, av, PA(j, k), l2, lim, o1, o2);
+                    bp_pe2_p2(l1, bp_comb<GMODE>(l2, r2v), av, PA(j, k), l2, lim, o1, o2);
                 else
-                    bp_pe2<GMODE, false, KEEP == 0 && GMODE == 0>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                    bp_pe2<GMODE, false, KEEP == 0 && GMODE == 3>(l1, bp_comb<GMODE>(l2, r2v), av, l2, lim, o1, o2);
                 const float back = __shfl_xor_sync(0xffffffffu, hi ? o1 : o2, msk); // my output the partner computed
                 Ln[k] = hi ? back : o1;
                 Ln[k + Q / 2] = hi ? o2 : back;
@@ -389,17 +388,17 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 const float av = RGET(j - 1, r1), r2v = RGET(j - 1, r2), l1 = LGET(j, r1), l2 = LGET(j, r2);
                 float o1, o2;
                 if (KEPT(j))
-                    bp_pe2_p2(l1, l2 + r2v, av, PA(j, ((r1 >> j) << (j - 1)) | (r1 & (h - 1))), l2, lim, o1, o2);
-                else if (GMODE == 0 && j == 1)
-                    bp_pe2_p2(l1, l2 + r2v, av, av != 0.0f ? pprior : 1.0f, l2, lim, o1, o2); // R[0] prior
+                    bp_pe2_p2(l1, bp_comb<GMODE>(l2, r2v), av, PA(j, ((r1 >> j) << (j - 1)) | (r1 & (h - 1))), l2, lim, o1, o2);
+                else if (GMODE == 3 && j == 1)
+                    bp_pe2_p2(l1, bp_comb<GMODE>(l2, r2v), av, av != 0.0f ? pprior : 1.0f, l2, lim, o1, o2); // R[0] prior
                 else
-                    bp_pe2<GMODE, false, KEEP == 0 && GMODE == 0>(l1, l2 + r2v, av, l2, lim, o1, o2);
+                    bp_pe2<GMODE, false, KEEP == 0 && GMODE == 3>(l1, bp_comb<GMODE>(l2, r2v), av, l2, lim, o1, o2);
                 if (j > 1) {
                     Lr[j - 2][r1] = o1;
                     Lr[j - 2][r2] = o2;
                 } else {
-                    su[r1] = o1 + av; // soft_u = L[0] + R[0]
-                    su[r2] = o2 + r2v;
+                    su[r1] = bp_comb<GMODE>(o1, av); // soft_u = L[0] + R[0]
+                    su[r2] = bp_comb<GMODE>(o2, r2v);
                 }
             }
         }
@@ -408,7 +407,7 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
             uint32_t syn = 0;
 #pragma unroll
             for (int r = 0; r < Q; ++r)
-                syn ^= (su[r] < 0.0f) ? col[r] : 0u;
+                syn ^= bp_neg<GMODE>(su[r]) ? col[r] : 0u;
             syn = __reduce_xor_sync(0xffffffffu, syn);
             if (lane == 0)
                 red[warp] = syn;
@@ -432,14 +431,14 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 for (int p = tid; p < N / 2; p += TPF) {
                     const int i1 = p, i2 = p + N / 2;
                     float o1, o2;
-                    bp_pe2<GMODE, true>(Rp[i1], Lch[i2] + Rp[i2], Lch[i1], Rp[i2], lim, o1, o2);
-                    ub[i1] = (Lch[i1] + o1) < 0.0f;
-                    ub[i2] = (Lch[i2] + o2) < 0.0f;
+                    bp_pe2<GMODE, true>(Rp[i1], bp_comb<GMODE>(Lch[i2], Rp[i2]), Lch[i1], Rp[i2], lim, o1, o2);
+                    ub[i1] = bp_neg<GMODE>(bp_comb<GMODE>(Lch[i1], o1));
+                    ub[i2] = bp_neg<GMODE>(bp_comb<GMODE>(Lch[i2], o2));
                 }
                 uint32_t v = 0;
 #pragma unroll
                 for (int r = 0; r < Q; ++r)
-                    v |= (su[r] < 0.0f ? 1u : 0u) << r;
+                    v |= (bp_neg<GMODE>(su[r]) ? 1u : 0u) << r;
 #pragma unroll
                 for (int h = 1; h < Q; h <<= 1)
                     v ^= (v >> h) & (h == 1 ? 0x55u : (h == 2 ? 0x33u : 0x0Fu));
@@ -476,12 +475,12 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
     }
 #pragma unroll
     for (int r = 0; r < Q; ++r)
-        ub[base + r] = su[r] < 0.0f;
+        ub[base + r] = bp_neg<GMODE>(su[r]);
     if (a.soft_u != nullptr) {
 #pragma unroll
         for (int r = 0; r < Q; r += 2)
             *reinterpret_cast<float2 *>(a.soft_u + (size_t)f * N + base + r) =
-                make_float2(su[r] * KOUT, su[r + 1] * KOUT);
+                make_float2(bp_store<GMODE>(su[r]), bp_store<GMODE>(su[r + 1]));
     }
     if constexpr (LOGN - 1 >= BW) {
         // soft_x = L[n] + R[n] (bp.py:164-168); R[n] is not needed by the sweeps,
@@ -492,9 +491,9 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
             for (int p = tid; p < N / 2; p += TPF) {
                 const int i1 = p, i2 = p + N / 2;
                 float o1, o2;
-                bp_pe2<GMODE, true>(Rp[i1], Lch[i2] + Rp[i2], Lch[i1], Rp[i2], lim, o1, o2);
-                a.soft_x[(size_t)f * N + i1] = (Lch[i1] + o1) * KOUT;
-                a.soft_x[(size_t)f * N + i2] = (Lch[i2] + o2) * KOUT;
+                bp_pe2<GMODE, true>(Rp[i1], bp_comb<GMODE>(Lch[i2], Rp[i2]), Lch[i1], Rp[i2], lim, o1, o2);
+                a.soft_x[(size_t)f * N + i1] = bp_store<GMODE>(bp_comb<GMODE>(Lch[i1], o1));
+                a.soft_x[(size_t)f * N + i2] = bp_store<GMODE>(bp_comb<GMODE>(Lch[i2], o2));
             }
         }
     } else {
@@ -513,11 +512,11 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
                 const float myR = hi ? Rh : Rk, myL = hi ? Lh : Lk;
                 const float av = hi ? pr : myR, r2v = hi ? myR : pr, l1 = hi ? pl : myL, l2 = hi ? myL : pl;
                 float o1, o2;
-                bp_pe2<GMODE, true>(av, l2 + r2v, l1, r2v, lim, o1, o2);
+                bp_pe2<GMODE, true>(av, bp_comb<GMODE>(l2, r2v), l1, r2v, lim, o1, o2);
                 const float back = __shfl_xor_sync(0xffffffffu, hi ? o1 : o2, msk);
                 const float rk = hi ? back : o1, rh = hi ? o2 : back; // R[n] at my nodes k, k + Q/2
-                a.soft_x[(size_t)f * N + base + k] = (Lk + rk) * KOUT;
-                a.soft_x[(size_t)f * N + base + k + Q / 2] = (Lh + rh) * KOUT;
+                a.soft_x[(size_t)f * N + base + k] = bp_store<GMODE>(bp_comb<GMODE>(Lk, rk));
+                a.soft_x[(size_t)f * N + base + k + Q / 2] = bp_store<GMODE>(bp_comb<GMODE>(Lh, rh));
             }
         }
     }
@@ -556,9 +555,18 @@ __global__ void __launch_bounds__(TPF) k_bp2(const BpArgs a)
 #undef PAP
 #undef KEPT
 
-static int bp2_default_tpf(int N)
+// Default threads per frame (measured, tools/bp_gmode_probe.py and
+// tools/bp_tpf_probe.py).  The likelihood-ratio form (g_mode 0) is fastest at
+// Q = 8 nodes per thread at every N (N=1024: 3265 / 3058 / 2568 Gg/s at 128 /
+// 256 / 512 threads); the re-encode stop needs R[n-1] in shared memory, i.e.
+// at least 64 threads.  The log-domain forms keep the round-1 settings.
+static int bp2_default_tpf(int N, int gmode, int stop_mode)
 {
-    return N >= 4096 ? 512 : (N / 4 >= 256 ? 256 : N / 4); // measured (tools/bp_tpf_probe.py)
+    if (gmode == 0) {
+        const int t = N / 8 > 32 ? N / 8 : 32;
+        return stop_mode == 1 && t < 64 ? 64 : t;
+    }
+    return N >= 4096 ? 512 : (N / 4 >= 256 ? 256 : N / 4);
 }
 
 static size_t bp2_smem_bytes(int logn, int tpf)
@@ -616,7 +624,7 @@ static int launch_bp2_n(const BpArgs &a, int tpf, cudaStream_t s)
     constexpr int LO = N / 8 > 32 ? N / 8 : 32; // Q <= 8 nodes per thread (Q = 16 needs ~120+ registers)
     constexpr int HI = N / 2;                   // Q >= 2
     if (tpf <= 0)
-        tpf = bp2_default_tpf(N);
+        tpf = bp2_default_tpf(N, GMODE, a.stop_mode);
     if (tpf < LO || tpf > HI)
         return PC_ERR_UNSUPPORTED;
 #define PC_BP2_CASE(T)                                                                                                 \
@@ -638,7 +646,7 @@ static int launch_bp2_n(const BpArgs &a, int tpf, cudaStream_t s)
 // re-encode stop at TPF = 32 and the kernel = 1 knob.
 // N = 4096 runs one 512-thread CTA per frame (Q = 8): 9 shared rows (144 KB),
 // no kept exponentials, one CTA per SM.
-bool bp2_eligible(const BpArgs &a, int tpf)
+bool bp2_eligible(const BpArgs &a, int g_mode, int tpf)
 {
     const int N = a.code.N;
     const int lo = N / 8 > 32 ? N / 8 : 32;
@@ -649,7 +657,7 @@ bool bp2_eligible(const BpArgs &a, int tpf)
     if (a.stop_mode != 1)
         return true;
     // the re-encode stop needs R[n-1] in shared memory: log2 TPF >= 6
-    const int t = tpf > 0 ? tpf : bp2_default_tpf(N);
+    const int t = tpf > 0 ? tpf : bp2_default_tpf(N, g_mode, a.stop_mode);
     return t >= 64;
 }
 
@@ -657,13 +665,24 @@ int launch_bp2(const BpArgs &a, int g_mode, int tpf, cudaStream_t s)
 {
     if (a.B == 0)
         return PC_OK;
-    if (!bp2_eligible(a, tpf) || (g_mode == 2 && a.stop_mode == 1))
+    if (!bp2_eligible(a, g_mode, tpf) || (g_mode == 2 && a.stop_mode == 1))
         return PC_ERR_UNSUPPORTED;
     const int n = a.code.n;
     if (g_mode == 2) { // exact g, per-g form (parity studies)
         switch (n) {
         case 10: return launch_bp2_n<10, 2>(a, tpf, s);
         case 11: return launch_bp2_n<11, 2>(a, tpf, s);
+        }
+        return PC_ERR_UNSUPPORTED;
+    }
+    if (g_mode == 3) { // the round-1 log-domain form (A/B knob)
+        switch (n) {
+        case 7: return launch_bp2_n<7, 3>(a, tpf, s);
+        case 8: return launch_bp2_n<8, 3>(a, tpf, s);
+        case 9: return launch_bp2_n<9, 3>(a, tpf, s);
+        case 10: return launch_bp2_n<10, 3>(a, tpf, s);
+        case 11: return launch_bp2_n<11, 3>(a, tpf, s);
+        case 12: return launch_bp2_n<12, 3>(a, tpf, s);
         }
         return PC_ERR_UNSUPPORTED;
     }

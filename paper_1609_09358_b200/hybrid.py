@@ -186,6 +186,7 @@ class HybridDecoder:
         # two kernels share the GPU instead of running back to back.
         self.s_scl = torch.cuda.Stream(device=dev, priority=-1) if overlap else self.s_bp
         self.kernel_events = None  # set to [] to time every K1 launch with CUDA events on the BP stream
+        self.scl_events = None  # set to [] to time every K2 + K3 pair with CUDA events on the SCL stream
         self.launches_per_chunk = 7  # 4 stamp kernels + K1 + K2 + K3 (memset nodes not counted)
         self._llr_dev = None
 
@@ -348,6 +349,9 @@ class HybridDecoder:
                 self.s_scl.wait_event(ev)
                 self._events.append(ev)
             chk(lib.pc_stamp(st.data_ptr() + 16, ss), "pc_stamp")
+            if self.scl_events is not None:
+                e2 = torch.cuda.Event(enable_timing=True)
+                e2.record(self.s_scl)
             q = self.queue.data_ptr() + 4 * b0
             cnt = self.counts.data_ptr() + 4 * c
             chk(lib.pc_compact(self.conv.data_ptr() + b0, nb, q, cnt, None, ss), "pc_compact")
@@ -359,6 +363,10 @@ class HybridDecoder:
                 ),
                 "pc_scl_decode",
             )
+            if self.scl_events is not None:
+                e3 = torch.cuda.Event(enable_timing=True)
+                e3.record(self.s_scl)
+                self.scl_events.append((e2, e3))
             chk(lib.pc_stamp(st.data_ptr() + 24, ss), "pc_stamp")
         self._B = B
         cur.wait_stream(self.s_bp)
