@@ -181,6 +181,11 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU baseline --
 _CPU_FRAMES: dict = {}
+# tools/ref_vs_port.py (8-core dev container, 256 frames per point, payloads identical)
+try:
+    PORT_OVER_REF = json.loads((ROOT / "profiles" / "ref_vs_port.json").read_text())["port_over_reference"]
+except Exception:
+    PORT_OVER_REF = float("nan")
 
 
 def cpu_hybrid_sample(frames_per_point: int, threads: int):
@@ -207,6 +212,14 @@ def cpu_hybrid_sample(frames_per_point: int, threads: int):
     return bits / busy / 1e9, busy
 
 
+def c3_config(frames: int, chunk: int, world: int) -> dict:
+    """The headline workload's config, shared by both arms (the reference arm
+    times a bounded sample of it, described in its cpu_baseline.sample)."""
+    return {"workload": WORKLOAD, "frames_per_point_per_gpu": frames, "ebno_db": list(EBNO), "chunk": chunk,
+            "parallelism": f"frame-sharded x{world}",
+            "l2": f"inputs larger than L2 ({frames * N * 4 / 1e6:.0f} MB per point)"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -222,12 +235,14 @@ def run_reference(args):
             vals.append((v, busy))
     value = float(np.mean([v for v, _ in vals]))
     ms = float(np.mean([b for _, b in vals])) * 1e3
-    sample = f"{fpp} frames per Eb/N0 point x {len(EBNO)} points per step (host PCG64 frames, fp64 oracle port)"
+    sample = (f"{fpp} frames per Eb/N0 point x {len(EBNO)} points per step (host PCG64 frames, fp64 oracle port on "
+              f"{threads} threads; the port is {PORT_OVER_REF:.2f}x the untouched Python reference on the same "
+              "frames and cores, profiles/ref_vs_port.json)")
     line = {
         "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOAD, "ebno_db": list(EBNO), "frames_per_point": fpp},
+        "config": c3_config(args.frames, args.chunk or args.frames, world),
         "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -323,6 +338,7 @@ def run_gpu(args):
         nat.check(lib.pc_count_errors(dec.payload.data_ptr(), msg[p].data_ptr(), B, m, errs[p].data_ptr(),
                                       nat.stream_handle()), "pc_count_errors")
     torch.cuda.synchronize()
+    latency_ops = latency_operating_points(torch, code, llr, dev) if rank == 0 else None
     # whole-job statistics: exact integer counters summed over the ranks (off
     # the timed path); the roofline below uses this rank's own iterations and
     # its own K1 time
@@ -403,10 +419,9 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (device Philox-keyed BPSK/AWGN frames, resident in HBM before timing)",
-            "config": {"workload": WORKLOAD, "frames_per_point_per_gpu": B, "ebno_db": list(EBNO),
-                       "chunk": dec.chunk, "parallelism": f"frame-sharded x{world}",
-                       "l2": f"inputs larger than L2 ({B * N * 4 / 1e6:.0f} MB per point)"},
+            "config": c3_config(B, dec.chunk, world),
             "p50_latency_ms": float(np.median([s["p50_latency_ms"] for s in sweep])),
+            "latency_operating_points": latency_ops,
             "sweep": sweep,
             "roofline": roofline,
             "k3": k3,
@@ -419,6 +434,44 @@ def run_gpu(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+def latency_operating_points(torch, code, llr, dev):
+    """p50 frame latency under the reference's semantic (a frame's latency runs
+    from its BP batch's start to its final decision, hybrid.py:56-66, sim.py:199)
+    at small batches: chunks of 32 frames (the reference's bp_batch_size) and
+    1024 frames over 4096 frames per point, and one frame alone on the GPU
+    (64 single-frame runs per point).  Untimed for the headline value."""
+    from paper_1609_09358_b200 import BpConfig, HybridDecoder, SclConfig
+
+    out = []
+    pts = [p for p, eb in enumerate(EBNO) if eb in (1.0, 2.0, 3.0, 4.0)]
+    NF = min(4096, llr.shape[1])
+    for ch in (32, 1024):
+        d = HybridDecoder(code, BpConfig(i_max=IMAX), SclConfig(LIST), capacity=NF, chunk=ch, device=dev)
+        for p in pts:
+            d.run(llr[p], NF).sync()  # warm-up
+            t0 = time.perf_counter()
+            d.run(llr[p], NF).sync()
+            wall = time.perf_counter() - t0
+            r = d.host_results()
+            c = np.arange(NF) // ch
+            done = np.where(r["converged"], r["t_bp"], r["t_scl"])
+            lat = (done - r["stamps"][c, 0]) * 1e-6
+            out.append({"ebno_db": EBNO[p], "chunk": ch, "frames": NF, "p50_ms": float(np.median(lat)),
+                        "p99_ms": float(np.percentile(lat, 99)), "gbps_wall": NF * code.message_len / wall / 1e9})
+    d1 = HybridDecoder(code, BpConfig(i_max=IMAX), SclConfig(LIST), capacity=1, chunk=1, device=dev)
+    for p in pts:
+        lat = []
+        for f in range(65):
+            d1.run(llr[p][f:f + 1], 1).sync()
+            r = d1.host_results()
+            done = r["t_bp"][0] if r["converged"][0] else r["t_scl"][0]
+            if f:  # the first run is a warm-up
+                lat.append((done - r["stamps"][0, 0]) * 1e-6)
+        out.append({"ebno_db": EBNO[p], "chunk": 1, "frames": 64, "p50_ms": float(np.median(lat)),
+                    "p99_ms": float(np.percentile(lat, 99)), "note": "one frame alone on the GPU"})
+    return out
+
 
 # ------------------------------------------------------ secondary workloads --
 COMM = None  # device of the collective tensors (the GPU under NCCL, the CPU under gloo)

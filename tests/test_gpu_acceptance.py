@@ -128,3 +128,30 @@ def test_device_channel_uncoded_ber_is_q_function(eb):
     q = 0.5 * math.erfc(1.0 / sigma / math.sqrt(2.0))
     n = x.size
     assert abs(ber - q) < 5 * math.sqrt(q * (1 - q) / n) + 1e-6, (ber, q)
+
+
+def test_throughput_model_eq1_within_25_percent():
+    """Reference acceptance test 08 (test_acceptance.py:260-284) on the device
+    pipeline, at its exact configuration: N=1024 K=512 CRC-16, L=8, i_max=50,
+    768 frames in BP batches of 32, at 1.5 / 2 / 2.5 dB.  The measured
+    hybrid_decode_batch throughput must be within 25% of Eq. (1)
+    (hybrid.theoretical_throughput) evaluated on the measured BP and SCL
+    service rates and gamma."""
+    from paper_1609_09358_b200 import FrameJob, hybrid_decode_batch, theoretical_throughput
+
+    assert theoretical_throughput(123.0, 45.0, 0.0) == 123.0
+    assert theoretical_throughput(100.0, 1.0, 0.01) == pytest.approx(50.0)
+    code = CodeConfig(1024, 512, crc=16)
+    gaps = []
+    for point, eb in enumerate((1.5, 2.0, 2.5)):
+        sigma = ebno_to_sigma(eb, code.rate)
+        jobs = []
+        for f in range(768):
+            m, llr = make_frame(code, sigma, frame_rng(800_000 + point, point, f))
+            jobs.append(FrameJob(frame_id=f, llrs=llr, true_message=m))
+        kw = dict(bp_batch_size=32, n_scl_workers=2)
+        hybrid_decode_batch([FrameJob(frame_id=j.frame_id, llrs=j.llrs, true_message=j.true_message) for j in jobs],
+                            code, BpConfig(i_max=50), SclConfig(8), **kw)  # warm-up (allocations, module load)
+        st = hybrid_decode_batch(jobs, code, BpConfig(i_max=50), SclConfig(8), **kw)
+        gaps.append(abs(st.t_hyb_theo_bps - st.throughput_bps) / st.t_hyb_theo_bps)
+    assert max(gaps) < 0.25, f"Eq. (1) gaps {gaps}"

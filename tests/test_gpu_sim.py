@@ -67,3 +67,66 @@ def test_cli_no_timing_is_byte_identical_to_reference_fixture(golden_meta, tmp_p
                "--out", str(out)])
     assert rc == 0
     assert out.read_text() == golden_meta["fixtures"]["no_timing"]["raw"]
+
+
+def _oracle_counts(code, llrs, msgs, L):
+    import numpy as np
+
+    import oracle
+
+    u, _, _ = oracle.scl_batch(llrs.astype(np.float32).astype(np.float64), code, L)
+    dec = u[:, code.info_positions][:, : code.message_len]
+    errs = (dec != msgs).sum(axis=1)
+    return int((errs > 0).sum()), int(errs.sum())
+
+
+def test_sc_decoder_point_matches_oracle():
+    """`decoder="sc"` through sim.run_point (reference sim.py:152-153: SC is
+    SCL with list size 1) on 1500 keyed frames equals the oracle's L = 1 on the
+    same frames: frame and bit error counts exactly."""
+    from paper_1609_09358_b200.channel import ebno_to_sigma, make_frames
+    from paper_1609_09358_b200.sim import run_point
+
+    cfg = SimConfig(N=256, k=128, decoder="sc", crc_width=0, ebno_points=(1.5,), min_frame_errors=10**6,
+                    max_frames=1500, master_seed=5)
+    rec = run_point(cfg, 1.5)
+    code = cfg.build_code()
+    msgs, llrs = make_frames(code, ebno_to_sigma(1.5, code.rate), 5, 0, 0, 1500)
+    fe, be = _oracle_counts(code, llrs, msgs, 1)
+    assert (rec.frames, rec.frame_errors, rec.bit_errors) == (1500, fe, be)
+    assert fe > 50  # the point is not trivially error-free
+
+
+def test_frozen_file_point_and_cli_match_oracle(tmp_path):
+    """A frozen set from a file (reference polar.py:317-328, cli.py:44):
+    a non-default mask (Bhattacharyya design at 0.1, then two positions
+    swapped) saved with save_frozen_mask drives sim.run_point and the CLI; the
+    device SCL (L = 4, CRC-16) counts equal the oracle's on the same frames
+    decoded with the same mask."""
+    import numpy as np
+
+    from paper_1609_09358_b200 import construct_frozen_mask, save_frozen_mask
+    from paper_1609_09358_b200.channel import ebno_to_sigma, make_frames
+    from paper_1609_09358_b200.cli import main
+    from paper_1609_09358_b200.sim import run_point
+
+    mask = construct_frozen_mask(256, 128, 0.1).copy()
+    fz, nf = np.flatnonzero(mask == 1), np.flatnonzero(mask == 0)
+    mask[fz[-1]], mask[nf[0]] = 0, 1  # still N - k frozen, no longer the default design
+    path = tmp_path / "mask.txt"
+    save_frozen_mask(mask, path)
+    cfg = SimConfig(N=256, k=128, decoder="scl", list_size=4, crc_width=16, frozen_file=str(path),
+                    ebno_points=(1.5,), min_frame_errors=10**6, max_frames=1200, master_seed=9)
+    code = cfg.build_code()
+    assert np.array_equal(code.frozen_mask, mask)
+    rec = run_point(cfg, 1.5)
+    msgs, llrs = make_frames(code, ebno_to_sigma(1.5, code.rate), 9, 0, 0, 1200)
+    fe, be = _oracle_counts(code, llrs, msgs, 4)
+    assert (rec.frames, rec.frame_errors, rec.bit_errors) == (1200, fe, be)
+    out = tmp_path / "sweep.csv"
+    rc = main(["--n", "256", "--k", "128", "--frozen-file", str(path), "--decoder", "scl", "--list-size", "4", "--ebno-list",
+               "1.5", "--seed", "9", "--min-frame-errors", "1000000", "--max-frames", "1200", "--no-timing",
+               "--out", str(out)])
+    assert rc == 0
+    row = out.read_text().strip().splitlines()[-1].split(",")
+    assert (int(row[1]), int(row[2]), int(row[3])) == (1200, be, fe)

@@ -7,26 +7,30 @@
 # into profiles/.
 TAG=${1:-rXX}
 OUT=gpurun_out
-if [ "$2" == "--summarize" ]; then
+summarize() {
+  # the judged summaries of this run into $DEST (on the box: gpurun_out/<tag>_profiles,
+  # merged back; the .ncu-rep files are too large to travel back all at once)
+  DEST=$1
+  mkdir -p $DEST
   for w in c3 c1 c2 c4 c5 ref; do
-    [ -s $OUT/${TAG}_bench_$w.json ] && grep '^{' $OUT/${TAG}_bench_$w.json | tail -1 > profiles/${TAG}_bench_$w.json
+    [ -s $OUT/${TAG}_bench_$w.json ] && grep '^{' $OUT/${TAG}_bench_$w.json | tail -1 > $DEST/${TAG}_bench_$w.json
   done
-  cp $OUT/${TAG}_launches.csv profiles/${TAG}_launches.csv
-  python tools/summarize_profiles.py launches $OUT/${TAG}_launches.csv > profiles/${TAG}_launches_summary.txt
+  cp $OUT/${TAG}_launches.csv $DEST/${TAG}_launches.csv
+  python tools/summarize_profiles.py launches $OUT/${TAG}_launches.csv > $DEST/${TAG}_launches_summary.txt
   python tools/summarize_profiles.py full $OUT/${TAG}_bp.ncu-rep \
     "$TAG: K1 N=1024 (c3 kernel), ncu --set full --clock-control none, tools/profile_kernels.py 16384 256 2.0" \
-    > profiles/${TAG}_ncu_bp.txt
+    > $DEST/${TAG}_ncu_bp.txt
   python tools/summarize_profiles.py full $OUT/${TAG}_bp4096.ncu-rep \
-    "$TAG: K1 N=4096 (c4 kernel), tools/profile_kernels.py 2048 16 2.0 4096" > profiles/${TAG}_ncu_bp4096.txt
+    "$TAG: K1 N=4096 (c4 kernel), tools/profile_kernels.py 2048 16 2.0 4096" > $DEST/${TAG}_ncu_bp4096.txt
   python tools/summarize_profiles.py full $OUT/${TAG}_bp128.ncu-rep \
-    "$TAG: K1 N=128 (c1 kernel), tools/profile_kernels.py 65536 16 2.0 128" > profiles/${TAG}_ncu_bp128.txt
-  python tools/sass_mix.py $OUT/${TAG}_bp.ncu-rep 30 > profiles/${TAG}_bp_sass_mix.txt
+    "$TAG: K1 N=128 (c1 kernel), tools/profile_kernels.py 65536 16 2.0 128" > $DEST/${TAG}_ncu_bp128.txt
+  python tools/sass_mix.py $OUT/${TAG}_bp.ncu-rep 30 > $DEST/${TAG}_bp_sass_mix.txt
   python tools/summarize_profiles.py full $OUT/${TAG}_scl.ncu-rep \
-    "$TAG: K3 N=1024 L=32 (c3 kernel), tools/profile_kernels.py 16 4096 1.5" > profiles/${TAG}_ncu_scl.txt
-  tail -3 $OUT/${TAG}_pytest.log > profiles/${TAG}_pytest_gpu.txt
-  python - "$OUT" "$TAG" <<'PY'
+    "$TAG: K3 N=1024 L=32 (c3 kernel), tools/profile_kernels.py 16 4096 1.5" > $DEST/${TAG}_ncu_scl.txt
+  tail -3 $OUT/${TAG}_pytest.log > $DEST/${TAG}_pytest_gpu.txt
+  python - "$OUT" "$TAG" "$DEST" <<'PY'
 import csv, io, json, subprocess, sys
-out, tag = sys.argv[1], sys.argv[2]
+out, tag, dest = sys.argv[1], sys.argv[2], sys.argv[3]
 def raw(rep):
     rows = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
                                                       capture_output=True, text=True).stdout)))
@@ -56,10 +60,13 @@ for name, N, frames in (("bp", 1024, 16384), ("bp4096", 4096, 2048), ("bp128", 1
         json.dump({"kernel": kern, "frames_per_launch": frames, "dram_bytes_per_launch": tot,
                    "dram_bytes_per_frame": tot / frames, "algorithmic_bytes_per_frame": 4173,
                    "source": f"profiles/{tag}_ncu_bp.txt ({tag}_bp.ncu-rep)"},
-                  open("profiles/bp_kernel_ncu.json", "w"), indent=1)
-json.dump(issue, open("profiles/k1_issue.json", "w"), indent=1)
+                  open(dest + "/bp_kernel_ncu.json", "w"), indent=1)
+json.dump(issue, open(dest + "/k1_issue.json", "w"), indent=1)
 print(json.dumps(issue, indent=1))
 PY
+}
+if [ "$2" == "--summarize" ]; then
+  cp $OUT/${TAG}_profiles/* profiles/
   exit 0
 fi
 mkdir -p $OUT
@@ -82,3 +89,7 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_sc
   python tools/profile_kernels.py 16 4096 1.5 > /dev/null 2>&1
 ls -la $OUT | grep $TAG
 for w in c3 ref c1 c2 c4 c5; do tail -c 400 $OUT/${TAG}_bench_$w.json; echo; done
+summarize $OUT/${TAG}_profiles
+# keep the K1 N=1024 report (for the source page); the others are summarized above
+rm -f $OUT/${TAG}_bp4096.ncu-rep $OUT/${TAG}_bp128.ncu-rep $OUT/${TAG}_scl.ncu-rep
+ls -la $OUT/${TAG}_profiles
