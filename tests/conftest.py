@@ -16,10 +16,40 @@ if str(ROOT) not in sys.path:
 GOLDEN = Path(__file__).resolve().parent / "golden"
 REF_SRC = Path("/root/reference/pkg/src")
 
+# ---- the reference's own test suite (tests/ref_suite) ----
+# tests/ref_suite/vendor.py copies /root/reference/pkg/tests/*.py, unmodified,
+# into the git-ignored tests/ref_suite/vendor/; they import ``polarsim``, the
+# test-only alias of this package in tests/ref_suite/polarsim/.  Every vendored
+# test is marked ``gpu`` (the decoders run on the device; on a CPU host they
+# raise NativeUnavailable by design) and ``ref_suite``.  Failures that follow
+# from the documented fp32 device arithmetic are strict xfails, with the cause
+# here and in DESIGN.md section 4.
+REF_SUITE = Path(__file__).resolve().parent / "ref_suite"
+if str(REF_SUITE) not in sys.path:
+    sys.path.insert(0, str(REF_SUITE))
+# the reference's CLI test runs `python -m polarsim` in a subprocess
+os.environ["PYTHONPATH"] = os.pathsep.join([str(REF_SUITE), str(ROOT)] +
+                                           [p for p in [os.environ.get("PYTHONPATH")] if p])
+REF_XFAIL: dict[str, str] = {}
+
+
+def pytest_collection_modifyitems(config, items):
+    vend = REF_SUITE / "vendor"
+    for it in items:
+        path = Path(str(it.fspath))
+        if vend not in path.parents:
+            continue
+        it.add_marker(pytest.mark.gpu)
+        it.add_marker(pytest.mark.ref_suite)
+        key = f"{path.name}::{it.name}"
+        if key in REF_XFAIL:
+            it.add_marker(pytest.mark.xfail(reason=REF_XFAIL[key], strict=True))
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and libpolarcuda.so")
     config.addinivalue_line("markers", "slow: long-running statistical check")
+    config.addinivalue_line("markers", "ref_suite: the reference's own tests (tests/ref_suite) on this package")
 
 
 @pytest.fixture(scope="session")
@@ -37,12 +67,19 @@ def reference():
     """The live reference package, only where /root/reference exists."""
     if not REF_SRC.exists():
         pytest.skip("reference tree not present (GPU box); golden fixtures cover it")
-    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_tests")
-    if str(REF_SRC) not in sys.path:
-        sys.path.append(str(REF_SRC))
-    import polarsim
+    # (its own numba cache: entries written under the module name "polarsim" do not load as "polarsim_ref")
+    os.environ["NUMBA_CACHE_DIR"] = "/tmp/numba_cache_polarsim_ref"
+    # loaded under its own name: "polarsim" is the test-only alias of this
+    # package that the vendored reference suite imports (tests/ref_suite)
+    if "polarsim_ref" not in sys.modules:
+        import importlib.util
 
-    return polarsim
+        spec = importlib.util.spec_from_file_location("polarsim_ref", REF_SRC / "polarsim" / "__init__.py",
+                                                      submodule_search_locations=[str(REF_SRC / "polarsim")])
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules["polarsim_ref"] = mod
+        spec.loader.exec_module(mod)
+    return sys.modules["polarsim_ref"]
 
 
 def unpack(packed, L):

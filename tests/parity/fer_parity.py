@@ -13,6 +13,12 @@ point:
     must overlap the oracle's.
 
     python tests/parity/fer_parity.py [--frames 2000] [--device-frames 131072] [--out profiles/fer_parity.json]
+
+With --frames above --chunk (default 65536) the paired frames are generated,
+decoded on both sides and counted chunk by chunk (10^6 paired frames per
+point fit in host memory), e.g. the high-SNR floor check
+    python tests/parity/fer_parity.py --frames 1000000 --ebno 3,3.5,4 --device-frames 0 \
+        --out profiles/fer_parity_1e6.json
 """
 
 from __future__ import annotations
@@ -59,10 +65,20 @@ def _frames(args):
     return np.array([o[0] for o in out]), np.array([o[1] for o in out]).astype(np.float32)
 
 
-def host_frames(point, ebno, count, workers):
-    chunks = [(point, ebno, s, min(256, count - s)) for s in range(0, count, 256)]
+def _frames_batch(args):
+    point, ebno, first, count = args
+    from paper_1609_09358_b200 import CodeConfig
+    from paper_1609_09358_b200.channel import ebno_to_sigma, make_frames
+
+    code = CodeConfig(N, K, crc=16)
+    msgs, llrs = make_frames(code, ebno_to_sigma(ebno, code.rate), SEED, point, first, count)
+    return msgs, llrs.astype(np.float32)
+
+
+def host_frames(point, ebno, count, workers, first=0):
+    chunks = [(point, ebno, first + s, min(2048, count - s)) for s in range(0, count, 2048)]
     with ProcessPoolExecutor(workers) as ex:
-        parts = list(ex.map(_frames, chunks))
+        parts = list(ex.map(_frames_batch, chunks))
     return np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
 
 
@@ -71,6 +87,7 @@ def main():
     ap.add_argument("--frames", type=int, default=2000)
     ap.add_argument("--device-frames", type=int, default=131072)
     ap.add_argument("--ebno", default="1,1.5,2,2.5,3,3.5,4")
+    ap.add_argument("--chunk", type=int, default=65536)
     ap.add_argument("--out", default=str(ROOT / "profiles" / "fer_parity.json"))
     args = ap.parse_args()
 
@@ -90,15 +107,24 @@ def main():
     all_ok = True
     for p, eb in enumerate(float(x) for x in args.ebno.split(",")):
         t0 = time.time()
-        msgs, llr32 = host_frames(p, eb, args.frames, threads)
-        cap = max(args.frames, args.device_frames)
+        cap = max(min(args.frames, args.chunk), args.device_frames)
         dec = HybridDecoder(code, BpConfig(i_max=IMAX), SclConfig(L), capacity=cap)
-        dec.run(torch.from_numpy(llr32).cuda(), args.frames).sync()
-        r = dec.host_results()
-        dev_pay = nat.unpack_bits(r["payload"], m)
-        ref_pay, ref_prov, _ = oracle.hybrid_batch(llr32.astype(np.float64), code, i_max=IMAX, L=L, nthreads=threads)
-        dev_err = (dev_pay != msgs).sum(axis=1)
-        ref_err = (ref_pay != msgs).sum(axis=1)
+        dev_err, ref_err, flips = [], [], 0
+        t_oracle = 0.0
+        for first in range(0, args.frames, args.chunk):
+            nb = min(args.chunk, args.frames - first)
+            msgs, llr32 = host_frames(p, eb, nb, threads, first)
+            dec.run(torch.from_numpy(llr32).cuda(), nb).sync()
+            r = dec.host_results()
+            dev_pay = nat.unpack_bits(r["payload"], m)
+            t1 = time.time()
+            ref_pay, ref_prov, _ = oracle.hybrid_batch(llr32.astype(np.float64), code, i_max=IMAX, L=L,
+                                                       nthreads=threads)
+            t_oracle += time.time() - t1
+            dev_err.append((dev_pay != msgs).sum(axis=1))
+            ref_err.append((ref_pay != msgs).sum(axis=1))
+            flips += int((~r["converged"][:nb] != ref_prov).sum())
+        dev_err, ref_err = np.concatenate(dev_err), np.concatenate(ref_err)
         fd, fr = int((dev_err > 0).sum()), int((ref_err > 0).sum())
         lo, hi = clopper_pearson(fr, args.frames)
         a = int(((dev_err > 0) & (ref_err == 0)).sum())
@@ -108,6 +134,18 @@ def main():
         ber_r = cluster_ci(ref_err, m)
         # larger device-only sample (Philox frames)
         B = args.device_frames
+        if B == 0:
+            inside = lo <= fd / args.frames <= hi
+            all_ok &= inside and pval > 0.01
+            pt = {"ebno_db": eb, "frames": args.frames, "frame_errors_device": fd, "frame_errors_oracle": fr,
+                  "fer_device": fd / args.frames, "fer_oracle": fr / args.frames, "fer_oracle_ci95": [lo, hi],
+                  "fer_device_ci95": list(clopper_pearson(fd, args.frames)), "device_fer_inside_oracle_ci": inside,
+                  "discordant_device_only": a, "discordant_oracle_only": b, "sign_test_p": pval,
+                  "provenance_flips": flips, "ber_device": ber_d, "ber_oracle": ber_r,
+                  "oracle_seconds": t_oracle, "seconds": time.time() - t0}
+            report["points"].append(pt)
+            print(json.dumps(pt), flush=True)
+            continue
         llr = torch.empty((B, N), dtype=torch.float32, device="cuda")
         mw = torch.empty((B, (m + 31) // 32), dtype=torch.int32, device="cuda")
         dc = nat.device_code(code)
@@ -128,7 +166,7 @@ def main():
             "fer_device": fd / args.frames, "fer_oracle": fr / args.frames, "fer_oracle_ci95": [lo, hi],
             "device_fer_inside_oracle_ci": inside,
             "discordant_device_only": a, "discordant_oracle_only": b, "sign_test_p": pval,
-            "provenance_flips": int((~r["converged"][:args.frames] != ref_prov).sum()),
+            "provenance_flips": flips,
             "ber_device": ber_d, "ber_oracle": ber_r,
             "device_only": {"frames": B, "fer": big_fe / B, "fer_ci95": [blo, bhi], "overlaps_oracle_ci": overlap},
             "seconds": time.time() - t0,
