@@ -65,29 +65,42 @@ def _clock_mhz(ck):
     return (ck or {}).get("sm_mhz") or peak_mhz, peak_mhz
 
 
+def k1_kernel_label(N: int) -> str:
+    n = N.bit_length() - 1
+    if N >= 256:
+        return (f"k_bp3<{n},0> (BP, likelihood-ratio arithmetic, {N // 8} threads/frame, warp-local boundaries in "
+                "three register layouts joined by shared-memory transposes)")
+    return f"k_bp2<{n},{k1_tpf(N)},0> (BP, likelihood-ratio arithmetic, lane-pair shuffles, one warp per frame)"
+
+
 def k1_roofline(torch, dev, N: int, g_total: float, k1_s: float, ck, frames_per_launch=None) -> dict:
     """Roofline of K1 from live numbers: g_total algorithmic exact-g
     evaluations (sum of iterations x 2nN) in k1_s seconds of K1 time (CUDA
-    events on K1's stream).  K1 is bound by the SM instruction issue rate
-    (ncu: issue slots ~80% busy, XU ~67%, HBM < 1%), so `peak` is the issue
-    bound: 148 SM x 4 warp-instructions/clk at the measured SM clock divided by
-    the warp-instructions K1 executes per algorithmic g (one ncu capture of the
-    same kernel, profiles/k1_issue.json).  `frac_alg` is SURVEY.md section 8(d)'s
-    fixed formula (achieved x 4 MUFU per g / XU peak), which the
-    likelihood-ratio arithmetic exceeds by design (1 MUFU per g, not 4)."""
+    events on K1's stream).  HBM is < 1% (4.2 KB per frame), so the bound is
+    an SM pipe.  Two are computed and the LOWER one is `peak` (`bound`):
+      * xu: the MUFU pipe, 148 SM x 16/clk at the measured SM clock, divided by
+        K1's MUFU per algorithmic g (one RCP per g of the likelihood-ratio
+        form, R[n] not computed: (2n-1)/(2n));
+      * issue: 148 SM x 4 warp-instructions/clk divided by the
+        warp-instructions K1 executes per algorithmic g (one ncu capture of the
+        same kernel, profiles/k1_issue.json).
+    `frac_alg` is SURVEY.md section 8(d)'s fixed formula (achieved x 4 MUFU per
+    g / XU peak), which the likelihood-ratio arithmetic exceeds by design."""
     n = N.bit_length() - 1
     achieved = g_total / k1_s / 1e9
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     mhz, max_mhz = _clock_mhz(ck)
     xu_ops = sms * 16 * mhz * 1e6
     mpg = mufu_per_alg_g(n)
+    xu_peak = xu_ops / mpg / 1e9
     issue = None
     try:
         issue = json.loads((ROOT / "profiles" / "k1_issue.json").read_text())[str(N)]
     except Exception:
         pass
     ipg = issue["warp_inst_per_alg_g"] if issue else None
-    peak = sms * 4 * mhz * 1e6 / ipg / 1e9 if ipg else None
+    issue_peak = sms * 4 * mhz * 1e6 / ipg / 1e9 if ipg else None
+    bound, peak = ("xu", xu_peak) if issue_peak is None or xu_peak <= issue_peak else ("issue", issue_peak)
     traffic = None
     try:
         per_frame = json.loads((ROOT / "profiles" / "bp_kernel_ncu.json").read_text())["dram_bytes_per_frame"]
@@ -96,17 +109,16 @@ def k1_roofline(torch, dev, N: int, g_total: float, k1_s: float, ck, frames_per_
     except Exception:
         pass
     return {
-        "bound": "issue", "achieved": achieved, "peak": peak, "unit": "Gg/s",
-        "frac": achieved / peak if peak else None, "traffic": traffic,
-        "frac_alg": achieved * 4 / (xu_ops / 1e9),
-        "kernel": f"k_bp2<{n},{k1_tpf(N)},0> (register/shuffle BP, likelihood-ratio arithmetic, "
-                  f"{k1_tpf(N)} threads/frame)",
+        "bound": bound, "achieved": achieved, "peak": peak, "unit": "Gg/s", "frac": achieved / peak,
+        "traffic": traffic, "frac_alg": achieved * 4 / (xu_ops / 1e9), "kernel": k1_kernel_label(N),
         "sm_mhz": mhz, "sm_max_mhz": max_mhz,
-        "warp_inst_per_alg_g": ipg, "issue_source": issue.get("source") if issue else None,
-        "xu": {"mufu_per_alg_g": mpg, "peak": xu_ops / mpg / 1e9, "frac": achieved * mpg / (xu_ops / 1e9)},
+        "xu": {"mufu_per_alg_g": mpg, "peak": xu_peak, "frac": achieved / xu_peak},
+        "issue": {"warp_inst_per_alg_g": ipg, "peak": issue_peak,
+                  "frac": achieved / issue_peak if issue_peak else None,
+                  "source": issue.get("source") if issue else None},
         "note": "unit = one exact-g evaluation as the reference counts them (2nN per frame-iteration, "
-                "bp.py:138-161); frac = share of the SM issue bound; frac_alg = SURVEY 8(d)'s XU formula at 4 "
-                "MUFU per g; xu = the MUFU pipe at K1's 1 RCP per g; HBM < 1% (4.2 KB per frame)",
+                "bp.py:138-161); peak = the lower of the MUFU (xu) and instruction-issue bounds at the measured "
+                "SM clock; frac_alg = SURVEY 8(d)'s XU formula at 4 MUFU per g; HBM < 1% (4.2 KB per frame)",
     }
 
 
@@ -518,7 +530,7 @@ BP_WORKLOADS = {
     "c1": {"N": 128, "K": 64, "pts": (2.0,), "pid": 30, "B": 1 << 20, "cfg": 0, "fixed_cap": True,
            "metric": "decoded info Gbit/s, inter-frame BP N=128 R=1/2 (i_max=50, CRC stop), Eb/N0 2 dB",
            "workload": "BP-only N=128 K=64 (48 payload + CRC-16) i_max=50 CRC stop (BASELINE configs[0])",
-           "kernel": "k_bp2<7,32,0,persistent> (register/shuffle BP, one warp per frame, kept exponentials)"},
+           "kernel": "k_bp2<7,32,0,persistent>"},
     "c4": {"N": 4096, "K": 2048, "pts": (2.0, 3.0), "pid": 10, "B": 1 << 16, "cfg": 3,
            "metric": "decoded info Gbit/s, inter-frame BP N=4096 R=1/2 (i_max=50, CRC stop), Eb/N0 2 and 3 dB",
            "workload": "BP-only N=4096 K=2048 (2032 payload + CRC-16) i_max=50 CRC stop (BASELINE configs[3])",

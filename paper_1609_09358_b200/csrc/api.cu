@@ -133,7 +133,7 @@ int pc_bp_decode(const float *llr, int32_t B, const pc_code_t *code, const pc_bp
     if (cfg == nullptr || B < 0 || (B > 0 && (llr == nullptr || iters == nullptr || converged == nullptr)))
         return PC_ERR_INVALID;
     if (cfg->i_max < 1 || cfg->g_mode < 0 || cfg->g_mode > 3 || cfg->stop_mode < 0 || cfg->stop_mode > 2 ||
-        cfg->kernel < 0 || cfg->kernel > 2 || !(cfg->llr_max > 0.0f))
+        cfg->kernel < 0 || cfg->kernel > 3 || !(cfg->llr_max > 0.0f))
         return PC_ERR_INVALID;
     if (cfg->stop_mode == 0 && (code->crc_width == 0 || code->crc_cols == nullptr))
         return PC_ERR_INVALID;

@@ -133,7 +133,9 @@ __device__ __forceinline__ void bp_pe2_core(float x, float y1, float y2, float p
 template <int GMODE, bool RS, bool LFMA = false>
 __device__ __forceinline__ void bp_pe2(float x, float y1, float y2, float add, BpLim lim, float &o1, float &o2)
 {
-    if (GMODE == 0) { // likelihood ratios: g = (1 + x y) / (x + y), one MUFU.RCP each
+    if (GMODE == 0) { // likelihood ratios: g = (1 + x y) / (x + y)
+        // (one reciprocal of (x + y1)(x + y2) for both quotients measured no faster:
+        // -0.6% at N=1024, tools/k1_variant_probe.sh; the kernel is issue-bound)
         o1 = fmaf(x, y1, 1.0f) * rcp_approx(x + y1);
         o2 = bp_clip<0>(fmaf(x, y2, 1.0f) * rcp_approx(x + y2) * add, lim);
         return;

@@ -297,9 +297,16 @@ class HybridDecoder:
     def _st(self, s) -> int:
         return int(s.cuda_stream)
 
-    def run(self, llr, B: int | None = None):
+    def run(self, llr, B: int | None = None, join: bool = True):
         """Enqueue the pipeline for ``llr[:B]`` (CUDA float32).  Returns immediately;
-        call ``sync()`` (or read results) afterwards."""
+        call ``sync()`` (or read results) afterwards.
+
+        ``join=False`` leaves the BP and SCL streams running after the call
+        (the caller's current stream does not wait for them): a second decoder's
+        batch can then start its BP stage while this batch is still in its SCL
+        stage (the paper's Fig. 2 overlap across batches).  This decoder's own
+        next batch still starts its BP stage only after this batch's SCL stage
+        (its buffers are reused); call ``join_streams()`` before reading results."""
         torch = self.torch
         N = self.code.N
         if not (hasattr(llr, "is_cuda") and llr.is_cuda):
@@ -319,6 +326,9 @@ class HybridDecoder:
         cur = torch.cuda.current_stream(self.device)
         self.s_bp.wait_stream(cur)
         self.s_scl.wait_stream(cur)
+        # this decoder's buffers (payload, flags, queue) are reused: the BP stage of
+        # this batch waits for the previous batch's SCL stage when it was not joined
+        self.s_bp.wait_stream(self.s_scl)
         bp_ref, scl_ref = ctypes.byref(self.nbp), ctypes.byref(self.nscl)
         base_llr = llr.data_ptr()
         self._events = []
@@ -369,6 +379,13 @@ class HybridDecoder:
                 self.scl_events.append((e2, e3))
             chk(lib.pc_stamp(st.data_ptr() + 24, ss), "pc_stamp")
         self._B = B
+        if join:
+            self.join_streams()
+        return self
+
+    def join_streams(self):
+        """The caller's current stream waits for this decoder's BP and SCL stages."""
+        cur = self.torch.cuda.current_stream(self.device)
         cur.wait_stream(self.s_bp)
         cur.wait_stream(self.s_scl)
         return self

@@ -30,7 +30,19 @@ if str(REF_SUITE) not in sys.path:
 # the reference's CLI test runs `python -m polarsim` in a subprocess
 os.environ["PYTHONPATH"] = os.pathsep.join([str(REF_SUITE), str(ROOT)] +
                                            [p for p in [os.environ.get("PYTHONPATH")] if p])
-REF_XFAIL: dict[str, str] = {}
+_FP32 = ("fp64 exact-equality assertion on device fp32 arithmetic (north_star: BP/SCL messages within 1e-4 "
+         "relative in fp32); measured on the B200: ")
+REF_XFAIL: dict[str, str] = {
+    # test_bp.py:126-141: assert_array_equal of iterate_once messages against the
+    # scalar fp64 restatement (reference_impls.py:154-188)
+    "test_bp.py::test_iteration_matches_scalar_reference": _FP32 + "max |diff| 4.5e-7, max relative 1.2e-7",
+    # test_bp.py:144-152: hand trace at abs=1e-15
+    "test_bp.py::test_first_sweep_hand_trace_n2": _FP32 + "4.99999952 vs 4.99999969 (|diff| 1.7e-7)",
+    # test_scl.py:200-214: metric against a brute-force fp64 forced-path metric at
+    # abs=1e-12; the WINNER (the minimum-metric codeword) is the same, only the
+    # fp32 metric value differs (8e-8)
+    "test_scl.py::test_metric_minimal_among_all_messages": _FP32 + "4.99495935 vs 4.99495944 (|diff| 8.2e-8)",
+}
 
 
 def pytest_collection_modifyitems(config, items):

@@ -36,9 +36,8 @@ def test_workload_lines(wl, frames):
     assert d["gpu_launches"] >= 1
     if wl in ("c1", "c3", "c4"):
         r = d["roofline"]
-        assert r["bound"] == "issue" and r["achieved"] > 0 and r["frac_alg"] > 0
-        assert r["frac"] is None or 0 < r["frac"] < 1.05
-        assert 0 < r["xu"]["frac"] < 1.0
+        assert r["bound"] in ("issue", "xu") and r["achieved"] > 0 and r["frac_alg"] > 0
+        assert 0 < r["frac"] < 1.05 and 0 < r["xu"]["frac"] < 1.0
         assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     if wl == "c1":
         assert d["fixed_cap"]["stop_mode"] == "none" and d["fixed_cap"]["frac_alg"] > 0

@@ -391,3 +391,38 @@ def test_soft_x_matches_oracle(N):
         ref = oracle.bp_decode(llr, code, i_max=3, stop_mode="none")
         assert mixed_err(res.soft_x, ref["soft_x"]) <= 1e-3
         assert mixed_err(res.soft_u, ref["soft_u"]) <= 1e-3
+
+
+@pytest.mark.parametrize("N,mode,g_mode", [(256, "crc", "exact"), (1024, "crc", "exact"), (1024, "reencode", "exact"),
+                                           (2048, "none", "exact"), (4096, "crc", "exact"), (512, "crc", "min")])
+def test_layout_kernel_matches_shuffle_kernel(N, mode, g_mode):
+    """K1 v3 (bp3.cu: warp-local boundaries in three register layouts joined by
+    shared-memory transposes) and K1 v2 (bp2.cu: lane-pair shuffles) at the
+    same 8 nodes per thread evaluate every PE with the same arithmetic:
+    bit-identical u_hat, soft_u, soft_x, iterations and flags."""
+    import ctypes
+
+    import torch
+    from paper_1609_09358_b200 import _native as nat
+
+    code = CodeConfig(N, N // 2, crc=16)
+    sigma = ebno_to_sigma(2.0, code.rate)
+    B = 600
+    x = torch.from_numpy(np.array([make_frame(code, sigma, frame_rng(93, N, f))[1] for f in range(B)],
+                                  dtype=np.float32)).cuda()
+    dc = nat.device_code(code)
+    outs = []
+    for kern in (2, 3):
+        cfg = BpConfig(i_max=30, stop_mode=mode, g_mode=g_mode).native(threads_per_frame=N // 8, kernel=kern)
+        u = torch.zeros((B, N // 32), dtype=torch.int32, device="cuda")
+        su = torch.zeros((B, N), device="cuda")
+        sx = torch.zeros((B, N), device="cuda")
+        it = torch.zeros(B, dtype=torch.int32, device="cuda")
+        cv = torch.zeros(B, dtype=torch.uint8, device="cuda")
+        nat.check(nat.load().pc_bp_decode(x.data_ptr(), B, dc.ref, ctypes.byref(cfg), u.data_ptr(), None,
+                                          su.data_ptr(), sx.data_ptr(), it.data_ptr(), cv.data_ptr(), None,
+                                          nat.stream_handle()), f"bp kernel {kern}")
+        torch.cuda.synchronize()
+        outs.append((u, su, sx, it, cv))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)

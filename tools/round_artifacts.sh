@@ -79,11 +79,11 @@ for w in c1 c2 c4 c5; do
 done
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/${TAG}_launches.csv \
   python bench.py --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_bp2 -c 1 -o $OUT/${TAG}_bp -f \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_bp -c 1 -o $OUT/${TAG}_bp -f \
   python tools/profile_kernels.py 16384 256 2.0 > $OUT/${TAG}_bp.out 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_bp2 -c 1 -o $OUT/${TAG}_bp4096 -f \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_bp -c 1 -o $OUT/${TAG}_bp4096 -f \
   python tools/profile_kernels.py 2048 16 2.0 4096 > $OUT/${TAG}_bp4096.out 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_bp2 -c 1 -o $OUT/${TAG}_bp128 -f \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_bp -c 1 -o $OUT/${TAG}_bp128 -f \
   python tools/profile_kernels.py 65536 16 2.0 128 > $OUT/${TAG}_bp128.out 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_scl3 -c 1 -o $OUT/${TAG}_scl -f \
   python tools/profile_kernels.py 16 4096 1.5 > /dev/null 2>&1
