@@ -101,9 +101,10 @@ typedef struct pc_bp_cfg {
 /* SclConfig, scl.py:39-66.  L in {1,2,4,8,16,32}.  virtual_levels: how many of
  * the top tree levels are recomputed from the channel instead of stored
  * (-1 = library default); a performance knob that does not change results.
- * warps_per_cta: 1..4 (0 = 1).  kernel: 0 = auto (v3 register-block kernel
- * for N >= 16, else v2), 1 = v2 (per-leaf shared-memory kernel), 2 = v3;
- * performance knobs that do not change results. */
+ * warps_per_cta: 1..4 (0 = 1).  kernel: 0 = auto (L = 1 and N >= 64: the
+ * one-warp-per-frame SC kernel; else the v3 register-block kernel for N >= 64,
+ * else v2), 1 = v2 (per-leaf shared-memory kernel), 2 = v3, 3 = the SC kernel
+ * (L = 1 only); performance knobs that do not change results. */
 typedef struct pc_scl_cfg {
     int32_t L, metric_exact, f_exact, selector_bitonic, virtual_levels, warps_per_cta;
     int32_t kernel;

@@ -205,8 +205,13 @@ int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32
     a.t_done = t_done;
     a.work = reinterpret_cast<int32_t *>(workspace);
     a.tbg = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(workspace) + 256);
-    if (cfg->kernel < 0 || cfg->kernel > 2)
+    if (cfg->kernel < 0 || cfg->kernel > 3)
         return PC_ERR_INVALID;
+    // L = 1 (SC): one warp per frame (sc1.cu), bit-identical to K3 v3 at L = 1
+    if (L == 1 && (cfg->kernel == 3 || (cfg->kernel == 0 && sc1_eligible(a))))
+        return sc1_eligible(a) ? launch_sc1(a, (cudaStream_t)stream) : PC_ERR_UNSUPPORTED;
+    if (cfg->kernel == 3)
+        return PC_ERR_UNSUPPORTED;
     int nv = cfg->virtual_levels;
     if (cfg->kernel != 1 && scl3_eligible(a, L)) {
         if (nv < 0)

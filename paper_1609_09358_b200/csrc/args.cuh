@@ -55,6 +55,8 @@ bool scl3_eligible(const SclArgs &a, int L);
 int scl3_prepare(SclArgs &a, int L, int nv_req);
 int launch_scl3(const SclArgs &a, int L, int wpc, cudaStream_t s);
 int64_t scl3_workspace_bytes(const SclArgs &a, int L, int wpc);
+bool sc1_eligible(const SclArgs &a);
+int launch_sc1(const SclArgs &a, cudaStream_t s);
 int launch_compact(const uint8_t *conv, int B, int32_t *queue, int32_t *count, cudaStream_t s);
 int launch_gen(const Code &c, uint64_t seed, int point, int64_t frame0, int B, float sigma, uint32_t *msg, float *llr,
                cudaStream_t s);
