@@ -1,22 +1,28 @@
 // sc1.cu -- K3 for list size 1 (successive cancellation, reference sim.py:152-153:
-// SC is scl_decode with L = 1): one WARP per frame (sm_100a).
+// SC is scl_decode with L = 1): G frames per warp, 32/G lanes per frame (sm_100a).
 //
 // K3 v3 (scl3.cuh) maps 32 / L frames onto a warp, one lane per path, so at
 // L = 1 every lane walks a whole frame alone: the upper tree levels (2^s
-// elements each) run serially per lane, 32 channel rows stream through L1/L2
-// per warp, and one frame takes ~0.8 ms at N = 2048.  Here the 32 lanes of a
-// warp share one frame:
-//   * the channel row is staged in the warp's shared memory;
-//   * every upper level (5 .. n-1) is computed element-parallel by the warp
-//     (lane t: elements t, t + 32, ...), f or g with the stored partial sums;
-//   * each block of 32 leaves runs on lane 0 from registers with the same leaf
-//     code as K3 v3 (levels 4..0, their partial sums in one word, the fp32
-//     metric and the L = 1 decision rule c1 < c0 of the (metric, index) order,
-//     _kernels.py:247-311), so decisions, metric and CRC flag are bit-identical
-//     to K3 v3 at L = 1 (tests/test_gpu_scl.py);
+// elements each) run serially per lane, the virtual top levels re-read 32
+// channel rows through L1/L2 per warp, and one frame takes ~0.9 ms at
+// N = 2048.  Here a group of GL = 32/G lanes shares one frame:
+//   * every upper level (5 .. n-1) is stored once per frame in shared memory
+//     and computed element-parallel by the group (lane t of the group:
+//     elements t, t + GL, ...), f or g with the stored partial sums; the
+//     channel row is read (coalesced, from global memory) only for level n-1;
+//   * each block of 32 leaves runs on the group's first lane from registers
+//     with the same leaf code as K3 v3 (levels 4..0, their partial sums in one
+//     word, the fp32 metric and the L = 1 decision rule c1 < c0 of the
+//     (metric, index) order, _kernels.py:247-311), so decisions, metric and
+//     CRC flag are bit-identical to K3 v3 at L = 1 (tools/sc1_ab.py,
+//     tests/test_gpu_scl.py);
 //   * the block's codeword is folded into the stored partial sums
-//     element-parallel.
-// Shared memory per warp: channel N floats, levels 5..n-1 (N - 32 floats),
+//     element-parallel;
+//   * the code tables (CRC syndrome columns, frozen and decision-aided words)
+//     are staged once per CTA in shared memory, so a leaf's column read is not
+//     a global-memory round trip on the decision chain.
+// G = 1 is the latency form (one frame per warp, small batches); G = 4 the
+// throughput form.  Shared memory per frame: levels 5..n-1 (N - 32 floats),
 // partial sums N/32 words, decisions N/32 words.
 #include "args.cuh"
 #include "scl_math.cuh"
@@ -27,169 +33,288 @@ namespace sc1 {
 constexpr int T = 5; // leaf blocks of 32
 __host__ __device__ constexpr int lvl(int s) { return (1 << s) - 32; }      // level s >= 5, floats
 __host__ __device__ constexpr int pso(int s) { return (1 << (s - 5)) - 1; } // partial sums of level s >= 5, words
-__host__ __device__ inline int warp_floats(int N) { return 2 * N + 2 * (N / 32) + 4; }
+// Stored LLR levels 5..TP = min(n - 1, 8); the NV = n - 1 - TP levels above are
+// recomputed from the channel (scl_math.cuh::virt_top) when the descent
+// crosses them (each of levels 9..n-1 is visited 2^(n-1-s) times per frame), so
+// a frame needs 2.5 KB of shared memory at N = 2048 instead of 8.5 KB.
+__host__ __device__ constexpr int top_level(int n) { return n - 1 < 8 ? n - 1 : 8; }
+__host__ __device__ inline int frame_words(int N, int n) // levels, partial sums, decisions, 32 leaf LLRs
+{
+    return (2 << top_level(n)) - 32 + 2 * (N / 32) + 32;
+}
+__host__ __device__ inline int table_words(int N) { return N + 2 * (N / 32); } // columns, frozen, da
 } // namespace sc1
 
-template <bool FEX>
+// One block of 32 leaves from its level-5 LLRs x (K3 v3's leaf code at L = 1):
+// decisions bu, the fp32 metric, the CRC syndrome and the block codeword betaT.
+// SPEC = false: the exact rule at every leaf (decision c1 < c0 of the metric
+// sums, _kernels.py:247-311), one dependent chain through MUFU and the metric.
+// SPEC = true: the decision chain takes u = (lam < 0) at info leaves (what the
+// rule decides unless metric + inc0 and metric + inc1 round to the same fp32
+// value), keeping the MUFU work and the metric off it; a second, unrolled pass
+// then evaluates the exact rule from the stored leaf LLRs and returns false if
+// any decision would differ (the caller replays the block with SPEC = false),
+// so the result is bit-identical either way.
+// One leaf j of a 32-leaf block (K3 v3's leaf code at L = 1): the leaf LLR from
+// the register levels, the decision and the partial-sum fold.  SPEC: the
+// decision u = (lam < 0) at info leaves and the LLR kept in lamS[j] for the
+// metric pass; else the exact rule (decision c1 < c0 of the fp32 metric sums,
+// _kernels.py:247-311) with the metric update.
+template <bool FEX, bool SPEC>
+__device__ __forceinline__ void leaf_step(int j, const float (&x)[32], float (&l4)[16], float (&l3)[8], float (&l2)[4],
+                                          float (&l1)[2], uint32_t &psr, uint32_t fzw, uint32_t daw, uint32_t col,
+                                          int metric_exact, float *lamS, float &metric, uint32_t &syn, uint32_t &bu,
+                                          uint32_t &betaT)
+{
+    float lam;
+    if (j & 1) {
+        lam = scl_g(l1[0], l1[1], psr & 1u);
+    } else {
+        if (j & 2) {
+            l1[0] = scl_g(l2[0], l2[2], (psr >> 1) & 1u);
+            l1[1] = scl_g(l2[1], l2[3], (psr >> 2) & 1u);
+        } else {
+            if (j & 4) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    l2[t] = scl_g(l3[t], l3[t + 4], (psr >> (3 + t)) & 1u);
+            } else {
+                if (j & 8) {
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        l3[t] = scl_g(l4[t], l4[t + 8], (psr >> (7 + t)) & 1u);
+                } else {
+                    if (j & 16) {
+#pragma unroll
+                        for (int t = 0; t < 16; ++t)
+                            l4[t] = scl_g(x[t], x[t + 16], (psr >> (15 + t)) & 1u);
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 16; ++t)
+                            l4[t] = scl_f<FEX>(x[t], x[t + 16]);
+                    }
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        l3[t] = scl_f<FEX>(l4[t], l4[t + 8]);
+                }
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    l2[t] = scl_f<FEX>(l3[t], l3[t + 4]);
+            }
+            l1[0] = scl_f<FEX>(l2[0], l2[2]);
+            l1[1] = scl_f<FEX>(l2[1], l2[3]);
+        }
+        lam = scl_f<FEX>(l1[0], l1[1]);
+    }
+    const uint32_t fz = (fzw >> j) & 1u, dz = (daw >> j) & 1u;
+    uint32_t u;
+    if constexpr (SPEC) {
+        // the decision the metric rule takes unless c0 and c1 round alike
+        u = (!fz && lam < 0.0f) ? 1u : 0u;
+        lamS[j] = lam;
+    } else {
+        float inc0, inc1;
+        metric_incs(lam, metric_exact, inc0, inc1);
+        if (fz | dz) {
+            u = (dz && lam < 0.0f) ? 1u : 0u;
+            metric += u ? inc1 : inc0;
+        } else {
+            // one path: keep the better child, a tie keeps u = 0 (candidate
+            // index 0 < 1, _kernels.py:253-267)
+            const float c0 = metric + inc0, c1 = metric + inc1;
+            u = c1 < c0 ? 1u : 0u;
+            metric = u ? c1 : c0;
+        }
+    }
+    if (!fz && u)
+        syn ^= col;
+    bu |= u << j;
+    // fold u into the register partial sums: level S = trailing ones of j
+    uint32_t Fw = u;
+    if (j & 1) {
+        Fw = ((psr ^ Fw) & 1u) | (Fw << 1);
+        if (j & 2) {
+            Fw = (((psr >> 1) ^ Fw) & 3u) | (Fw << 2);
+            if (j & 4) {
+                Fw = (((psr >> 3) ^ Fw) & 15u) | (Fw << 4);
+                if (j & 8) {
+                    Fw = (((psr >> 7) ^ Fw) & 255u) | (Fw << 8);
+                    if (j & 16)
+                        betaT = (((psr >> 15) ^ Fw) & 0xffffu) | (Fw << 16);
+                    else
+                        psr = (psr & ~(0xffffu << 15)) | (Fw << 15);
+                } else {
+                    psr = (psr & ~(255u << 7)) | (Fw << 7);
+                }
+            } else {
+                psr = (psr & ~(15u << 3)) | (Fw << 3);
+            }
+        } else {
+            psr = (psr & ~(3u << 1)) | (Fw << 1);
+        }
+    } else {
+        psr = (psr & ~1u) | Fw;
+    }
+}
+
+// One block of 32 leaves from its level-5 LLRs x: decisions bu, the fp32
+// metric, the CRC syndrome and the block codeword betaT.
+// SPEC = false: the exact rule at every leaf, one dependent chain through the
+// MUFU and the metric (one copy of the leaf code, runtime j).
+// SPEC = true: the decision chain takes u = (lam < 0) at info leaves, unrolled
+// so every branch on j and every partial-sum bit position is resolved at
+// compile time; a second, unrolled pass evaluates the exact rule from the kept
+// leaf LLRs and returns false if any decision would differ (the caller then
+// replays the block with SPEC = false): bit-identical either way.
+template <bool FEX, bool SPEC>
+__device__ __forceinline__ bool leaf_block(const float (&x)[32], uint32_t fzw, uint32_t daw, const uint32_t *cols,
+                                           int metric_exact, float *lamS, float &metric, uint32_t &syn, uint32_t &bu,
+                                           uint32_t &betaT)
+{
+    float l4[16], l3[8], l2[4], l1[2];
+    uint32_t psr = 0;
+    bu = 0;
+    if constexpr (SPEC) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            leaf_step<FEX, true>(j, x, l4, l3, l2, l1, psr, fzw, daw, cols[j], metric_exact, lamS, metric, syn, bu,
+                                 betaT);
+        bool same = true;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float lam = lamS[j];
+            const uint32_t fz = (fzw >> j) & 1u, dz = (daw >> j) & 1u, us = (bu >> j) & 1u;
+            float inc0, inc1;
+            metric_incs(lam, metric_exact, inc0, inc1);
+            if (fz | dz) {
+                metric += us ? inc1 : inc0;
+            } else {
+                const float c0 = metric + inc0, c1 = metric + inc1;
+                const uint32_t u = c1 < c0 ? 1u : 0u;
+                same &= u == us;
+                metric = u ? c1 : c0;
+            }
+        }
+        return same;
+    } else {
+#pragma unroll 1
+        for (int j = 0; j < 32; ++j)
+            leaf_step<FEX, false>(j, x, l4, l3, l2, l1, psr, fzw, daw, cols[j], metric_exact, lamS, metric, syn, bu,
+                                  betaT);
+        return true;
+    }
+}
+
+template <bool FEX, int G, int NV>
 __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
 {
     using namespace sc1;
     constexpr uint32_t FULL = 0xffffffffu;
-    extern __shared__ __align__(16) float smf[];
-    const int N = a.code.N, n = a.code.n;
-    const int lane = threadIdx.x & 31;
-    float *ch = smf + (size_t)(threadIdx.x >> 5) * warp_floats(N);
-    float *lv = ch + N;
-    uint32_t *ps = reinterpret_cast<uint32_t *>(lv + N);
-    uint32_t *ub = ps + N / 32;
-    const uint32_t *frzg = a.code.frozen_bits;
-    const uint32_t *damg = a.code.da_bits;
-    const uint32_t *colg = a.code.crc_cols;
+    constexpr int GL = 32 / G; // lanes per frame
+    extern __shared__ __align__(16) uint32_t smw[];
+    const int N = a.code.N, n = a.code.n, NW = N >> 5;
+    const int lane = threadIdx.x & 31, grp = lane / GL, pl = lane % GL;
+    uint32_t *colS = smw;
+    uint32_t *frzS = colS + N;
+    uint32_t *daS = frzS + NW;
     const bool use_crc = a.code.crc_width > 0;
+    for (int i = threadIdx.x; i < N; i += blockDim.x)
+        colS[i] = use_crc ? a.code.crc_cols[i] : 0u;
+    for (int i = threadIdx.x; i < NW; i += blockDim.x) {
+        frzS[i] = a.code.frozen_bits[i];
+        daS[i] = a.code.da_bits != nullptr ? a.code.da_bits[i] : 0u;
+    }
+    __syncthreads();
+    const int tp = NV > 0 ? 8 : n - 1; // top stored level
+    float *lv = reinterpret_cast<float *>(smw + table_words(N) + ((threadIdx.x >> 5) * G + grp) * frame_words(N, n));
+    uint32_t *ps = reinterpret_cast<uint32_t *>(lv + (2 << tp) - 32);
+    uint32_t *ub = ps + NW;
+    float *lam = reinterpret_cast<float *>(ub + NW); // 32 leaf LLRs of the current block
     const int total = a.count != nullptr ? *a.count : a.B;
     const int nblk = N >> T;
 
     for (;;) {
-        int qi = 0;
+        int base = 0;
         if (lane == 0)
-            qi = atomicAdd(a.work, 1);
-        qi = __shfl_sync(FULL, qi, 0);
-        if (qi >= total)
+            base = atomicAdd(a.work, G);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= total)
             break;
-        const int frame = a.queue != nullptr ? a.queue[qi] : qi;
-        {
-            const float4 *g = reinterpret_cast<const float4 *>(a.llr + (size_t)frame * N);
-            for (int t = lane; t < N / 4; t += 32)
-                reinterpret_cast<float4 *>(ch)[t] = __ldg(g + t);
-        }
-        __syncwarp();
+        const int qi = base + grp;
+        const bool live = qi < total;
+        const int frame = live ? (a.queue != nullptr ? a.queue[qi] : qi) : 0;
+        const float *ch = a.llr + (size_t)frame * N;
         float metric = 0.0f;
         uint32_t syn = 0u;
         for (int b = 0; b < nblk; ++b) {
             const int i0 = b << T;
-            // ---- upper descent: levels start..5, element-parallel ----
+            // ---- upper descent: levels start..5, element-parallel over the group ----
             const int start = (b == 0) ? n - 1 : T + __ffs(b) - 1;
-            for (int s = start; s >= T; --s) {
+            for (int s = start < tp ? start : tp; s >= T; --s) {
                 const int w = 1 << s;
-                const float *src = (s + 1 == n) ? ch : lv + lvl(s + 1);
                 float *dst = lv + lvl(s);
-                if ((i0 >> s) & 1) {
-                    const uint32_t *pw = ps + pso(s);
-                    for (int t = lane; t < w; t += 32)
-                        dst[t] = scl_g(src[t], src[t + w], (pw[t >> 5] >> (t & 31)) & 1u);
+                const bool g = (i0 >> s) & 1;
+                const uint32_t *pw = ps + pso(s);
+                if constexpr (NV > 0) {
+                    if (s == tp) { // (its source level tp + 1 is virtual)
+                        // level tp from the virtual levels n-NV..n-1 (recomputed from the channel)
+                        const uint32_t *psp[NV];
+                        uint32_t gm = 0;
+#pragma unroll
+                        for (int d = 0; d < NV; ++d) {
+                            psp[d] = ps + pso(n - NV + d);
+                            gm |= ((uint32_t)(i0 >> (n - NV + d)) & 1u) << d;
+                        }
+                        for (int t = pl; t < w; t += GL) {
+                            const float A = virt_top<NV, FEX>(ch, n, t, psp, gm);
+                            const float B = virt_top<NV, FEX>(ch, n, t + w, psp, gm);
+                            dst[t] = g ? scl_g(A, B, (pw[t >> 5] >> (t & 31)) & 1u) : scl_f<FEX>(A, B);
+                        }
+                        __syncwarp();
+                        continue;
+                    }
+                }
+                if (s + 1 == n) { // from the channel (global memory, coalesced)
+                    for (int t = pl; t < w; t += GL) {
+                        const float A = __ldg(ch + t), B = __ldg(ch + t + w);
+                        dst[t] = g ? scl_g(A, B, (pw[t >> 5] >> (t & 31)) & 1u) : scl_f<FEX>(A, B);
+                    }
                 } else {
-                    for (int t = lane; t < w; t += 32)
-                        dst[t] = scl_f<FEX>(src[t], src[t + w]);
+                    const float *src = lv + lvl(s + 1);
+                    for (int t = pl; t < w; t += GL) {
+                        const float A = src[t], B = src[t + w];
+                        dst[t] = g ? scl_g(A, B, (pw[t >> 5] >> (t & 31)) & 1u) : scl_f<FEX>(A, B);
+                    }
                 }
                 __syncwarp();
             }
-            // ---- the block's 32 leaves on lane 0, registers only (K3 v3's leaf code at L = 1) ----
+            // ---- the block's 32 leaves on the group's first lane, registers only
+            // (K3 v3's leaf code at L = 1) ----
             uint32_t betaT = 0;
-            if (lane == 0) {
+            if (pl == 0) {
                 float x[32];
 #pragma unroll
                 for (int t = 0; t < 32; t += 4) {
                     const float4 v = *reinterpret_cast<const float4 *>(lv + t);
                     x[t] = v.x, x[t + 1] = v.y, x[t + 2] = v.z, x[t + 3] = v.w;
                 }
-                const uint32_t fzw = __ldg(frzg + b);
-                const uint32_t daw = damg != nullptr ? __ldg(damg + b) : 0u;
-                float l4[16], l3[8], l2[4], l1[2];
-                uint32_t psr = 0, bu = 0;
-#pragma unroll 1
-                for (int j = 0; j < 32; ++j) {
-                    float lam;
-                    if (j & 1) {
-                        lam = scl_g(l1[0], l1[1], psr & 1u);
-                    } else {
-                        if (j & 2) {
-                            l1[0] = scl_g(l2[0], l2[2], (psr >> 1) & 1u);
-                            l1[1] = scl_g(l2[1], l2[3], (psr >> 2) & 1u);
-                        } else {
-                            if (j & 4) {
-#pragma unroll
-                                for (int t = 0; t < 4; ++t)
-                                    l2[t] = scl_g(l3[t], l3[t + 4], (psr >> (3 + t)) & 1u);
-                            } else {
-                                if (j & 8) {
-#pragma unroll
-                                    for (int t = 0; t < 8; ++t)
-                                        l3[t] = scl_g(l4[t], l4[t + 8], (psr >> (7 + t)) & 1u);
-                                } else {
-                                    if (j & 16) {
-#pragma unroll
-                                        for (int t = 0; t < 16; ++t)
-                                            l4[t] = scl_g(x[t], x[t + 16], (psr >> (15 + t)) & 1u);
-                                    } else {
-#pragma unroll
-                                        for (int t = 0; t < 16; ++t)
-                                            l4[t] = scl_f<FEX>(x[t], x[t + 16]);
-                                    }
-#pragma unroll
-                                    for (int t = 0; t < 8; ++t)
-                                        l3[t] = scl_f<FEX>(l4[t], l4[t + 8]);
-                                }
-#pragma unroll
-                                for (int t = 0; t < 4; ++t)
-                                    l2[t] = scl_f<FEX>(l3[t], l3[t + 4]);
-                            }
-                            l1[0] = scl_f<FEX>(l2[0], l2[2]);
-                            l1[1] = scl_f<FEX>(l2[1], l2[3]);
-                        }
-                        lam = scl_f<FEX>(l1[0], l1[1]);
-                    }
-                    const uint32_t fz = (fzw >> j) & 1u, dz = (daw >> j) & 1u;
-                    float inc0, inc1;
-                    metric_incs(lam, a.metric_exact, inc0, inc1);
-                    uint32_t u;
-                    if (fz | dz) {
-                        u = (dz && lam < 0.0f) ? 1u : 0u;
-                        metric += u ? inc1 : inc0;
-                    } else {
-                        // one path: keep the better child, a tie keeps u = 0 (candidate
-                        // index 0 < 1, _kernels.py:253-267)
-                        const float c0 = metric + inc0, c1 = metric + inc1;
-                        u = c1 < c0 ? 1u : 0u;
-                        metric = u ? c1 : c0;
-                    }
-                    if (!fz && u && use_crc)
-                        syn ^= __ldg(colg + i0 + j);
-                    bu |= u << j;
-                    // fold u into the register partial sums: level S = trailing ones of j
-                    uint32_t Fw = u;
-                    if (j & 1) {
-                        Fw = ((psr ^ Fw) & 1u) | (Fw << 1);
-                        if (j & 2) {
-                            Fw = (((psr >> 1) ^ Fw) & 3u) | (Fw << 2);
-                            if (j & 4) {
-                                Fw = (((psr >> 3) ^ Fw) & 15u) | (Fw << 4);
-                                if (j & 8) {
-                                    Fw = (((psr >> 7) ^ Fw) & 255u) | (Fw << 8);
-                                    if (j & 16)
-                                        betaT = (((psr >> 15) ^ Fw) & 0xffffu) | (Fw << 16);
-                                    else
-                                        psr = (psr & ~(0xffffu << 15)) | (Fw << 15);
-                                } else {
-                                    psr = (psr & ~(255u << 7)) | (Fw << 7);
-                                }
-                            } else {
-                                psr = (psr & ~(15u << 3)) | (Fw << 3);
-                            }
-                        } else {
-                            psr = (psr & ~(3u << 1)) | (Fw << 1);
-                        }
-                    } else {
-                        psr = (psr & ~1u) | Fw;
-                    }
+                const uint32_t fzw = frzS[b], daw = daS[b];
+                uint32_t bu = 0;
+                const float m0 = metric;
+                const uint32_t s0 = syn;
+                if (!leaf_block<FEX, true>(x, fzw, daw, colS + i0, a.metric_exact, lam, metric, syn, bu, betaT)) {
+                    metric = m0; // an info decision hinged on the metric's rounding: exact replay
+                    syn = s0;
+                    leaf_block<FEX, false>(x, fzw, daw, colS + i0, a.metric_exact, lam, metric, syn, bu, betaT);
                 }
                 ub[b] = bu;
             }
             // ---- block end: fold the block codeword into the stored partial sums ----
-            betaT = __shfl_sync(FULL, betaT, 0);
+            betaT = __shfl_sync(FULL, betaT, grp * GL);
             const int S = T + __ffs(~b) - 1; // level of the node this block completes
             if (S < n) {
                 const int words = 1 << (S - T);
-                for (int w = lane; w < words; w += 32) {
+                for (int w = pl; w < words; w += GL) {
                     uint32_t v = betaT;
                     for (int s = T; s < S; ++s)
                         if (((w >> (s - T)) & 1) == 0)
@@ -200,35 +325,34 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
             __syncwarp();
         }
         // ---- outputs (the one path is the winner, scl.py:177-191) ----
-        metric = __shfl_sync(FULL, metric, 0);
-        syn = __shfl_sync(FULL, syn, 0);
-        const int NW = N >> 5;
-        if (a.u_bits != nullptr)
-            for (int w = lane; w < NW; w += 32)
-                a.u_bits[(size_t)frame * NW + w] = ub[w];
-        if (a.payload != nullptr) {
-            const int m = a.code.m, MW = (m + 31) >> 5;
-            for (int bb = lane; bb < 32 * MW; bb += 32) {
-                uint32_t bit = 0u;
-                if (bb < m) {
-                    const int p = __ldg(a.code.info_pos + bb);
-                    bit = (ub[p >> 5] >> (p & 31)) & 1u;
+        metric = __shfl_sync(FULL, metric, grp * GL);
+        syn = __shfl_sync(FULL, syn, grp * GL);
+        if (live) {
+            if (a.u_bits != nullptr)
+                for (int w = pl; w < NW; w += GL)
+                    a.u_bits[(size_t)frame * NW + w] = ub[w];
+            if (a.payload != nullptr) {
+                const int m = a.code.m, MW = (m + 31) >> 5;
+                for (int w = pl; w < MW; w += GL) {
+                    uint32_t v = 0u;
+                    for (int q = 0; q < 32 && 32 * w + q < m; ++q) {
+                        const int p = __ldg(a.code.info_pos + 32 * w + q);
+                        v |= ((ub[p >> 5] >> (p & 31)) & 1u) << q;
+                    }
+                    a.payload[(size_t)frame * MW + w] = v;
                 }
-                const uint32_t v = __ballot_sync(FULL, bit);
-                if (lane == 0)
-                    a.payload[(size_t)frame * MW + (bb >> 5)] = v;
             }
-        }
-        if (lane == 0) {
-            const bool ok = use_crc && syn == a.code.crc_offset;
-            if (a.metric != nullptr)
-                a.metric[frame] = metric;
-            if (a.crc_ok != nullptr)
-                a.crc_ok[frame] = ok;
-            if (a.sel != nullptr)
-                a.sel[frame] = ok;
-            if (a.t_done != nullptr)
-                a.t_done[frame] = globaltimer();
+            if (pl == 0) {
+                const bool ok = use_crc && syn == a.code.crc_offset;
+                if (a.metric != nullptr)
+                    a.metric[frame] = metric;
+                if (a.crc_ok != nullptr)
+                    a.crc_ok[frame] = ok;
+                if (a.sel != nullptr)
+                    a.sel[frame] = ok;
+                if (a.t_done != nullptr)
+                    a.t_done[frame] = globaltimer();
+            }
         }
         __syncwarp();
     }
@@ -236,19 +360,20 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
 
 bool sc1_eligible(const SclArgs &a) { return a.code.n >= 6 && a.code.n <= 12; }
 
-int launch_sc1(const SclArgs &a, cudaStream_t s)
+template <bool FEX, int G, int NV>
+static int launch_sc1_t(const SclArgs &a, cudaStream_t s)
 {
-    if (a.B == 0)
-        return PC_OK;
-    if (cudaMemsetAsync(a.work, 0, sizeof(int32_t), s) != cudaSuccess)
-        return PC_ERR_CUDA;
-    auto kern = a.f_exact ? k_sc1<true> : k_sc1<false>;
-    const int N = a.code.N;
-    const size_t per_warp = (size_t)sc1::warp_floats(N) * 4;
+    auto kern = k_sc1<FEX, G, NV>;
+    const int N = a.code.N, n = a.code.n;
     int wpc = 4;
-    while (wpc > 1 && (size_t)wpc * per_warp > 200 * 1024)
-        --wpc;
-    const size_t smem = (size_t)wpc * per_warp;
+    auto bytes = [&](int w) {
+        return ((size_t)sc1::table_words(N) + (size_t)w * G * sc1::frame_words(N, n)) * 4;
+    };
+    while (wpc > 1 && bytes(wpc) > 227 * 1024)
+        wpc >>= 1;
+    const size_t smem = bytes(wpc);
+    if (smem > 227 * 1024)
+        return PC_ERR_UNSUPPORTED;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return PC_ERR_CUDA;
     int dev = 0, sms = 0, per_sm = 0;
@@ -257,11 +382,43 @@ int launch_sc1(const SclArgs &a, cudaStream_t s)
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpc, smem) != cudaSuccess || per_sm < 1)
         return PC_ERR_UNSUPPORTED;
     long long grid = (long long)sms * per_sm;
-    const long long need = ((long long)a.B + wpc - 1) / wpc; // one warp per frame at most
+    const long long need = ((long long)a.B + (long long)wpc * G - 1) / ((long long)wpc * G);
     if (grid > need)
         grid = need;
     kern<<<(int)grid, 32 * wpc, smem, s>>>(a);
     return cudaGetLastError() == cudaSuccess ? PC_OK : PC_ERR_CUDA;
+}
+
+template <bool FEX, int G>
+static int launch_sc1_g(const SclArgs &a, cudaStream_t s)
+{
+    switch (a.code.n > 9 ? a.code.n - 9 : 0) { // NV: virtual levels above level 8
+    case 0: return launch_sc1_t<FEX, G, 0>(a, s);
+    case 1: return launch_sc1_t<FEX, G, 1>(a, s);
+    case 2: return launch_sc1_t<FEX, G, 2>(a, s);
+    case 3: return launch_sc1_t<FEX, G, 3>(a, s);
+    }
+    return PC_ERR_UNSUPPORTED;
+}
+
+// G = 1 (latency form, one frame per warp) while the batch fits one frame per
+// resident warp, else SC1_G frames per warp (throughput form).
+#ifndef SC1_G
+#define SC1_G 8
+#endif
+int launch_sc1(const SclArgs &a, cudaStream_t s)
+{
+    if (a.B == 0)
+        return PC_OK;
+    if (cudaMemsetAsync(a.work, 0, sizeof(int32_t), s) != cudaSuccess)
+        return PC_ERR_CUDA;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const bool small = a.B <= sms * 8;
+    if (small)
+        return a.f_exact ? launch_sc1_g<true, 1>(a, s) : launch_sc1_g<false, 1>(a, s);
+    return a.f_exact ? launch_sc1_g<true, SC1_G>(a, s) : launch_sc1_g<false, SC1_G>(a, s);
 }
 
 } // namespace pc

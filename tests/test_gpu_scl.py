@@ -154,3 +154,38 @@ def test_crc_widths_vs_oracle(crc, L):
     ref_u, ref_m, ref_ok = oracle.scl_batch(llrs, code, L)
     got = scl_decode_batch(llrs, code, SclConfig(L))
     _compare(f"crc{crc}L{L}", ref_u, ref_m, ref_ok, got)
+
+
+@pytest.mark.parametrize("N,crc,fmode,mmode,da,B", [
+    (64, 8, "minsum", "exact", 0.0, 700), (256, None, "exact", "exact", 0.0, 700),
+    (1024, 16, "minsum", "approx", 0.0, 700), (2048, 16, "minsum", "exact", 0.3, 700),
+    (2048, 16, "minsum", "exact", 0.0, 3000), (4096, 24, "minsum", "exact", 0.0, 1300)])
+def test_sc_kernel_matches_list_kernel_at_l1(N, crc, fmode, mmode, da, B):
+    """The SC kernel (sc1.cu: 32/G lanes per frame, element-parallel upper
+    levels, speculative decision chain verified by the exact metric rule) is
+    bit-identical to K3 v3 at L = 1 (u_hat, metric, CRC flag, payload), in its
+    latency form (B <= 8 per SM: one frame per warp) and its throughput form."""
+    import os
+
+    import torch
+
+    code = CodeConfig(N, N // 2, crc=crc)
+    sigma = ebno_to_sigma(1.5, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(77, N, f))[1] for f in range(B)], dtype=np.float32)
+    x = torch.from_numpy(llrs).cuda()
+    cfg = SclConfig(1, metric_mode=mmode, f_mode=fmode, da_threshold=da)
+    outs = []
+    old = os.environ.get("PC_SCL_KERNEL")
+    try:
+        for kern in ("2", "3"):
+            os.environ["PC_SCL_KERNEL"] = kern
+            r = scl_decode_batch(x, code, cfg, payload=True)
+            torch.cuda.synchronize()
+            outs.append((r.u_hat, r.metric, r.crc_ok, r.payload_words))
+    finally:
+        if old is None:
+            os.environ.pop("PC_SCL_KERNEL", None)
+        else:
+            os.environ["PC_SCL_KERNEL"] = old
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)

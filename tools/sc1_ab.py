@@ -39,7 +39,7 @@ for N, crc in ((64, 8), (128, 16), (256, None), (1024, 16), (2048, 16), (4096, 2
     code = CodeConfig(N, N // 2, crc=crc)
     llr = frames(code, 1.5, 1500)
     for fm, mm, da in (("minsum", "exact", 0.0), ("exact", "exact", 0.0), ("minsum", "approx", 0.0),
-                       ("minsum", "exact", 2.0)):
+                       ("minsum", "exact", 0.3)):
         cfg = SclConfig(1, metric_mode=mm, f_mode=fm, da_threshold=da)
         a, b = dec(llr, code, cfg, 2), dec(llr, code, cfg, 3)
         same = [bool(torch.equal(x, y)) for x, y in ((a.u_hat, b.u_hat), (a.metric, b.metric),
