@@ -38,9 +38,9 @@ __host__ __device__ constexpr int pso(int s) { return (1 << (s - 5)) - 1; } // p
 // crosses them (each of levels 9..n-1 is visited 2^(n-1-s) times per frame), so
 // a frame needs 2.5 KB of shared memory at N = 2048 instead of 8.5 KB.
 __host__ __device__ constexpr int top_level(int n) { return n - 1 < 8 ? n - 1 : 8; }
-__host__ __device__ inline int frame_words(int N, int n) // levels, partial sums, decisions, 32 leaf LLRs
+__host__ __device__ inline int frame_words(int N, int n) // levels, partial sums, decisions, leaf LLRs, increments
 {
-    return (2 << top_level(n)) - 32 + 2 * (N / 32) + 32;
+    return (2 << top_level(n)) - 32 + 2 * (N / 32) + 96;
 }
 __host__ __device__ inline int table_words(int N) { return N + 2 * (N / 32); } // columns, frozen, da
 } // namespace sc1
@@ -157,17 +157,16 @@ __device__ __forceinline__ void leaf_step(int j, const float (&x)[32], float (&l
     }
 }
 
-// One block of 32 leaves from its level-5 LLRs x: decisions bu, the fp32
-// metric, the CRC syndrome and the block codeword betaT.
-// SPEC = false: the exact rule at every leaf, one dependent chain through the
-// MUFU and the metric (one copy of the leaf code, runtime j).
-// SPEC = true: the decision chain takes u = (lam < 0) at info leaves, unrolled
-// so every branch on j and every partial-sum bit position is resolved at
-// compile time; a second, unrolled pass evaluates the exact rule from the kept
-// leaf LLRs and returns false if any decision would differ (the caller then
-// replays the block with SPEC = false): bit-identical either way.
+// The decision chain of one block of 32 leaves from its level-5 LLRs x:
+// decisions bu, the CRC syndrome and the block codeword betaT.
+// SPEC = true: u = (lam < 0) at info leaves (what the exact rule decides unless
+// metric + inc0 and metric + inc1 round to the same fp32 value), the leaf LLRs
+// kept in lamS for the metric pass; unrolled, so every branch on j and every
+// partial-sum bit position is resolved at compile time.
+// SPEC = false: the exact rule with the metric at every leaf (the replay when
+// the metric pass rejects a speculative decision; one copy of the leaf code).
 template <bool FEX, bool SPEC>
-__device__ __forceinline__ bool leaf_block(const float (&x)[32], uint32_t fzw, uint32_t daw, const uint32_t *cols,
+__device__ __forceinline__ void leaf_chain(const float (&x)[32], uint32_t fzw, uint32_t daw, const uint32_t *cols,
                                            int metric_exact, float *lamS, float &metric, uint32_t &syn, uint32_t &bu,
                                            uint32_t &betaT)
 {
@@ -179,13 +178,28 @@ __device__ __forceinline__ bool leaf_block(const float (&x)[32], uint32_t fzw, u
         for (int j = 0; j < 32; ++j)
             leaf_step<FEX, true>(j, x, l4, l3, l2, l1, psr, fzw, daw, cols[j], metric_exact, lamS, metric, syn, bu,
                                  betaT);
-        bool same = true;
+    } else {
+#pragma unroll 1
+        for (int j = 0; j < 32; ++j)
+            leaf_step<FEX, false>(j, x, l4, l3, l2, l1, psr, fzw, daw, cols[j], metric_exact, lamS, metric, syn, bu,
+                                  betaT);
+    }
+}
+
+// The exact rule over a block from precomputed increments inc[2j] (u = 0),
+// inc[2j + 1] (u = 1): the metric in leaf order, and true if every
+// speculative decision in bu is what the rule decides (bit-identical result).
+__device__ __forceinline__ bool metric_pass(uint32_t fzw, uint32_t daw, uint32_t bu, const float *inc, float &metric)
+{
+    bool same = true;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const float lam = lamS[j];
-            const uint32_t fz = (fzw >> j) & 1u, dz = (daw >> j) & 1u, us = (bu >> j) & 1u;
-            float inc0, inc1;
-            metric_incs(lam, metric_exact, inc0, inc1);
+    for (int j = 0; j < 32; j += 2) {
+        const float4 v = *reinterpret_cast<const float4 *>(inc + 2 * j);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int jj = j + h;
+            const float inc0 = h ? v.z : v.x, inc1 = h ? v.w : v.y;
+            const uint32_t fz = (fzw >> jj) & 1u, dz = (daw >> jj) & 1u, us = (bu >> jj) & 1u;
             if (fz | dz) {
                 metric += us ? inc1 : inc0;
             } else {
@@ -195,14 +209,8 @@ __device__ __forceinline__ bool leaf_block(const float (&x)[32], uint32_t fzw, u
                 metric = u ? c1 : c0;
             }
         }
-        return same;
-    } else {
-#pragma unroll 1
-        for (int j = 0; j < 32; ++j)
-            leaf_step<FEX, false>(j, x, l4, l3, l2, l1, psr, fzw, daw, cols[j], metric_exact, lamS, metric, syn, bu,
-                                  betaT);
-        return true;
     }
+    return same;
 }
 
 template <bool FEX, int G, int NV>
@@ -230,6 +238,7 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
     uint32_t *ps = reinterpret_cast<uint32_t *>(lv + (2 << tp) - 32);
     uint32_t *ub = ps + NW;
     float *lam = reinterpret_cast<float *>(ub + NW); // 32 leaf LLRs of the current block
+    float *inc = lam + 32;                            // their metric increments (u = 0, u = 1)
     const int total = a.count != nullptr ? *a.count : a.B;
     const int nblk = N >> T;
 
@@ -244,8 +253,8 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
         const bool live = qi < total;
         const int frame = live ? (a.queue != nullptr ? a.queue[qi] : qi) : 0;
         const float *ch = a.llr + (size_t)frame * N;
-        float metric = 0.0f;
-        uint32_t syn = 0u;
+        float metric = 0.0f, m_blk = 0.0f; // m_blk, s_blk: metric and syndrome at the block's start
+        uint32_t syn = 0u, s_blk = 0u;
         for (int b = 0; b < nblk; ++b) {
             const int i0 = b << T;
             // ---- upper descent: levels start..5, element-parallel over the group ----
@@ -290,23 +299,38 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
             }
             // ---- the block's 32 leaves on the group's first lane, registers only
             // (K3 v3's leaf code at L = 1) ----
-            uint32_t betaT = 0;
-            if (pl == 0) {
-                float x[32];
+            uint32_t betaT = 0, bu = 0;
+            float x[32];
+            const uint32_t fzw = frzS[b], daw = daS[b];
+            if (pl == 0) { // the decision chain (speculative), leaf LLRs into lam[]
 #pragma unroll
                 for (int t = 0; t < 32; t += 4) {
                     const float4 v = *reinterpret_cast<const float4 *>(lv + t);
                     x[t] = v.x, x[t + 1] = v.y, x[t + 2] = v.z, x[t + 3] = v.w;
                 }
-                const uint32_t fzw = frzS[b], daw = daS[b];
-                uint32_t bu = 0;
-                const float m0 = metric;
-                const uint32_t s0 = syn;
-                if (!leaf_block<FEX, true>(x, fzw, daw, colS + i0, a.metric_exact, lam, metric, syn, bu, betaT)) {
-                    metric = m0; // an info decision hinged on the metric's rounding: exact replay
-                    syn = s0;
-                    leaf_block<FEX, false>(x, fzw, daw, colS + i0, a.metric_exact, lam, metric, syn, bu, betaT);
+                leaf_chain<FEX, true>(x, fzw, daw, colS + i0, a.metric_exact, lam, metric, syn, bu, betaT);
+            }
+            __syncwarp();
+            // the metric increments of the 32 leaves, element-parallel over the group
+            for (int j = pl; j < 32; j += GL) {
+                float i0v, i1v;
+                metric_incs(lam[j], a.metric_exact, i0v, i1v);
+                inc[2 * j] = i0v;
+                inc[2 * j + 1] = i1v;
+            }
+            __syncwarp();
+            if (pl == 0) {
+                // the exact rule from the increments: the metric, and whether every
+                // speculative decision stands
+                if (!metric_pass(fzw, daw, bu, inc, metric)) {
+                    // an info decision hinged on the metric's rounding: exact replay of the
+                    // block from its start (metric and syndrome as they were)
+                    metric = m_blk;
+                    syn = s_blk;
+                    leaf_chain<FEX, false>(x, fzw, daw, colS + i0, a.metric_exact, lam, metric, syn, bu, betaT);
                 }
+                m_blk = metric;
+                s_blk = syn;
                 ub[b] = bu;
             }
             // ---- block end: fold the block codeword into the stored partial sums ----
