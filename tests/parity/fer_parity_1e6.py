@@ -10,6 +10,9 @@ Two phases, so the slow side does not hold the GPU:
     python tests/parity/fer_parity_1e6.py device gpurun_out/fer1e6_device.npz
     # anywhere with cores: the oracle on the same frames (regenerated), compare
     python tests/parity/fer_parity_1e6.py oracle gpurun_out/fer1e6_device.npz profiles/fer_parity_1e6.json
+Options (both phases alike): --ebno 3,3.5,4 --frames 1000000 --point0 10, e.g. the
+full sweep at 2 x 10^4 paired frames per point:
+    ... device gpurun_out/fer20k_device.npz --ebno 1,1.5,2,2.5,3,3.5,4 --frames 20000 --point0 20
 """
 
 from __future__ import annotations
@@ -112,7 +115,18 @@ def oracle_phase(dev_file, out):
 
 
 if __name__ == "__main__":
-    if sys.argv[1] == "device":
-        device_phase(sys.argv[2])
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("phase", choices=("device", "oracle"))
+    ap.add_argument("files", nargs="+")
+    ap.add_argument("--ebno", default=",".join(str(e) for e in EBNO))
+    ap.add_argument("--frames", type=int, default=FRAMES)
+    ap.add_argument("--point0", type=int, default=POINT0)
+    args = ap.parse_args()
+    EBNO = tuple(float(x) for x in args.ebno.split(","))
+    FRAMES, POINT0 = args.frames, args.point0
+    if args.phase == "device":
+        device_phase(args.files[0])
     else:
-        sys.exit(oracle_phase(sys.argv[2], sys.argv[3]))
+        sys.exit(oracle_phase(args.files[0], args.files[1]))
