@@ -426,3 +426,37 @@ def test_layout_kernel_matches_shuffle_kernel(N, mode, g_mode):
         outs.append((u, su, sx, it, cv))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("N,mode", [(256, "crc"), (1024, "reencode"), (1024, "crc"), (2048, "none")])
+def test_all_bp_kernels_bit_identical(N, mode):
+    """With the likelihood-ratio arithmetic every BP kernel evaluates a PE with
+    the same bp_math.cuh::bp_pe2 on the same message values, so the
+    shared-memory kernel (kernel 1), the lane-shuffle kernel (2) and the layout
+    kernel (3) agree bit-for-bit: iterations, flags, u_hat and soft_u."""
+    import ctypes
+
+    import torch
+    from paper_1609_09358_b200 import _native as nat
+
+    code = CodeConfig(N, N // 2, crc=16)
+    sigma = ebno_to_sigma(2.0, code.rate)
+    B = 400
+    x = torch.from_numpy(np.array([make_frame(code, sigma, frame_rng(95, N, f))[1] for f in range(B)],
+                                  dtype=np.float32)).cuda()
+    dc = nat.device_code(code)
+    outs = []
+    for kern in (1, 2, 3):
+        cfg = BpConfig(i_max=30, stop_mode=mode).native(threads_per_frame=N // 8 if kern > 1 else 0, kernel=kern)
+        u = torch.zeros((B, N // 32), dtype=torch.int32, device="cuda")
+        su = torch.zeros((B, N), device="cuda")
+        it = torch.zeros(B, dtype=torch.int32, device="cuda")
+        cv = torch.zeros(B, dtype=torch.uint8, device="cuda")
+        nat.check(nat.load().pc_bp_decode(x.data_ptr(), B, dc.ref, ctypes.byref(cfg), u.data_ptr(), None,
+                                          su.data_ptr(), None, it.data_ptr(), cv.data_ptr(), None,
+                                          nat.stream_handle()), f"bp kernel {kern}")
+        torch.cuda.synchronize()
+        outs.append((u, su, it, cv))
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
