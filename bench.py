@@ -625,8 +625,11 @@ def run_bp_workload(args):
     conv_h = [torch.empty(B, dtype=torch.uint8, pin_memory=True) for _ in pts]
     # e2e units: each point's batch in NC chunks, NBUF chunk buffers, so the
     # first exposed copy is one chunk and the link streams ahead of the decode
-    NC, NBUF = (4, 3) if B % 4 == 0 else (1, 2)  # (8 chunks measured slower: launch tails)
+    NC = 4 if B % 4 == 0 else 1  # (8 chunks measured slower: launch tails)
     Bc = B // NC
+    # a deep ring of device input buffers (up to 6 GB of HBM): the link copies
+    # ahead through slow chunks, so it keeps pace where a decode is shorter than its copy
+    NBUF = max(2, min(args.steps * len(pts) * NC, 16, int(6e9 // (Bc * n4 * 4))))
     dbufs = [torch.empty((Bc, n4), dtype=torch.float32, device=dev) for _ in range(NBUF)]
     s_copy = torch.cuda.Stream(device=dev)
 

@@ -209,11 +209,15 @@ class HybridDecoder:
         torch.cuda.current_stream(self.device).synchronize()
         return self._pay_host[:B].numpy().view(np.uint32), self._conv_host[:B].numpy().astype(bool)
 
-    def decode_host_many(self, batches):
+    def decode_host_many(self, batches, input_bytes: float = 6e9):
         """End-to-end call over several HOST batches (pinned float32 [B_i, N]):
-        the H2D copies of batches i+1 and i+2 run on a copy stream while batch i
-        decodes (three device input buffers), and each batch's payload words and converged
-        flags are read back on the copy stream while the next batch decodes.  Returns a list of
+        the H2D copies of the next batches run on a copy stream while batch i
+        decodes (a ring of device input buffers, as many as ``input_bytes`` of
+        HBM holds, at least 3), and each batch's payload words and converged
+        flags are read back on a second copy stream (PCIe is full duplex) while
+        the next batch decodes.  A deep ring lets the link copy ahead through
+        the slow points of a sweep, so it keeps pace where a fast point's decode
+        is shorter than its copy.  Returns a list of
         (payload words uint32 [B_i, ceil(m/32)], converged bool [B_i]) numpy
         arrays, in order: views of pinned buffers that the next call reuses (copy
         them to keep them).  Results equal ``decode_host`` per batch."""
@@ -228,10 +232,13 @@ class HybridDecoder:
         # NBUF device input buffers: the copy of batch i+NBUF-1 starts while
         # batch i decodes, so the link keeps copying through short decodes
         # (a fast point's decode can be shorter than its PCIe copy).
-        NBUF = 3
-        if getattr(self, "_dbuf", None) is None or self._dbuf[0].shape[0] < self.capacity:
+        NBUF = max(3, min(len(batches), 16, int(input_bytes // (self.capacity * N * 4))))
+        if (getattr(self, "_dbuf", None) is None or self._dbuf[0].shape[0] < self.capacity
+                or len(self._dbuf) < NBUF):
             self._dbuf = [torch.empty((self.capacity, N), dtype=torch.float32, device=dev) for _ in range(NBUF)]
             self._s_copy = torch.cuda.Stream(device=dev)
+            self._s_back = torch.cuda.Stream(device=dev)
+        NBUF = len(self._dbuf)
         cur = torch.cuda.current_stream(dev)
         outs = []
         h2d = [None] * len(batches)
@@ -270,15 +277,16 @@ class HybridDecoder:
             ev.record(cur)
             done[i] = ev
             pay, conv = self._pinned_out(i, B)
-            with torch.cuda.stream(self._s_copy):
-                self._s_copy.wait_event(ev)
+            with torch.cuda.stream(self._s_back):
+                self._s_back.wait_event(ev)
                 pay.copy_(dec.payload[:B], non_blocking=True)
                 conv.copy_(dec.conv[:B], non_blocking=True)
                 e2 = torch.cuda.Event()
-                e2.record(self._s_copy)
+                e2.record(self._s_back)
             d2h[i] = e2
             outs.append((pay, conv))
         self._s_copy.synchronize()
+        self._s_back.synchronize()
         cur.synchronize()
         return [(p.numpy().view(np.uint32), c.numpy().view(np.bool_)) for p, c in outs]
 
