@@ -98,7 +98,8 @@ typedef struct pc_bp_cfg {
     int32_t *work;
 } pc_bp_cfg_t;
 
-/* SclConfig, scl.py:39-66.  L in {1,2,4,8,16,32}.  virtual_levels: how many of
+/* SclConfig, scl.py:39-66.  L in 1..32 (N >= 64 for L not a power of two: the
+ * v3 kernel keeps L paths on the next power of two of lanes).  virtual_levels: how many of
  * the top tree levels are recomputed from the channel instead of stored
  * (-1 = library default); a performance knob that does not change results.
  * warps_per_cta: 1..4 (0 = 1).  kernel: 0 = auto (L = 1 and N >= 64: the

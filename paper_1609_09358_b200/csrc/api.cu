@@ -184,9 +184,12 @@ int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32
         return rc;
     if (cfg == nullptr || B < 0 || workspace == nullptr || (B > 0 && llr == nullptr))
         return PC_ERR_INVALID;
-    const int L = cfg->L;
-    if (L < 1 || L > PC_MAX_LIST || (L & (L - 1)) != 0)
+    const int Lreq = cfg->L;
+    if (Lreq < 1 || Lreq > PC_MAX_LIST)
         return PC_ERR_UNSUPPORTED;
+    int L = 1; // lanes per frame: the next power of two (K3 v3 keeps Lreq paths on them)
+    while (L < Lreq)
+        L <<= 1;
     if (code->crc_width > 0 && code->crc_cols == nullptr)
         return PC_ERR_INVALID;
     SclArgs a;
@@ -197,6 +200,7 @@ int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32
     a.code = to_device_code(*code);
     a.metric_exact = cfg->metric_exact;
     a.f_exact = cfg->f_exact;
+    a.list_cap = Lreq;
     a.u_bits = u_bits;
     a.payload = payload;
     a.metric = metric;
@@ -221,7 +225,7 @@ int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32
             return rc3;
         return launch_scl3(a, L, cfg->warps_per_cta, (cudaStream_t)stream);
     }
-    if (cfg->kernel == 2)
+    if (cfg->kernel == 2 || L != Lreq) // (v2 takes power-of-two list sizes only)
         return PC_ERR_UNSUPPORTED;
     if (nv < 0)
         nv = code->n >= 12 ? 4 : (code->n >= 10 ? 3 : (code->n >= 8 ? 2 : 0));
@@ -231,18 +235,21 @@ int pc_scl_decode(const float *llr, int32_t B, const int32_t *queue, const int32
 
 int64_t pc_scl_workspace_bytes(const pc_code_t *code, const pc_scl_cfg_t *cfg)
 {
-    if (check_shape(code) || cfg == nullptr || cfg->L < 1 || cfg->L > PC_MAX_LIST || (cfg->L & (cfg->L - 1)))
+    if (check_shape(code) || cfg == nullptr || cfg->L < 1 || cfg->L > PC_MAX_LIST)
         return -1;
+    int L = 1;
+    while (L < cfg->L)
+        L <<= 1;
     SclArgs a{};
     a.code = to_device_code(*code);
     a.B = 1;
-    if (cfg->kernel != 1 && scl3_eligible(a, cfg->L)) {
+    if (cfg->kernel != 1 && scl3_eligible(a, L)) {
         int nv = cfg->virtual_levels;
         if (nv < 0)
             nv = code->n >= 10 ? 3 : (code->n >= 8 ? 2 : 0);
-        if (scl3_prepare(a, cfg->L, nv))
+        if (scl3_prepare(a, L, nv))
             return -1;
-        return scl3_workspace_bytes(a, cfg->L, cfg->warps_per_cta);
+        return scl3_workspace_bytes(a, L, cfg->warps_per_cta);
     }
     return pc_workspace_bytes();
 }

@@ -24,7 +24,8 @@ struct SclArgs {
     const int32_t *queue, *count;
     Code code;
     int32_t metric_exact, f_exact;
-    int32_t nv; // virtual top levels
+    int32_t list_cap; // the list size L (K3 v3 runs it on the next power of two of lanes)
+    int32_t nv;       // virtual top levels
     uint32_t *u_bits, *payload;
     float *metric;
     uint8_t *crc_ok, *sel;

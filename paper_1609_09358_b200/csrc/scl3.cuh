@@ -205,6 +205,9 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
     const bool ch_smem = a.o_ch >= 0;
 
     const int grp = lane / L, gbase = grp * L, pl = lane - gbase;
+    // the list size: L (the lanes per frame) or, for a list size that is not a
+    // power of two, fewer (lanes Lc..L-1 of a frame group never hold a path)
+    const int Lc = a.list_cap > 0 && a.list_cap < L ? a.list_cap : L;
     const uint32_t gmask_lo = (L == 32) ? FULL : ((1u << L) - 1u);
     const int total = a.count != nullptr ? *a.count : a.B;
     float *own = llr + lane * ss;
@@ -426,8 +429,7 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
                     const float c0 = act ? metric + inc0 : INFINITY;
                     const float c1 = act ? metric + inc1 : INFINITY;
                     bool k0 = act, k1 = act;
-                    bool need_rank = false;
-                    if (__any_sync(FULL, P == L)) {
+                    if (__any_sync(FULL, P == Lc)) {
                         // ---- selection at a full list: exactly the L best of 2L by (metric, index) ----
                         // (live groups share P; a finished group has P = 0 and takes no part)
                         // g = agreeing child, b = the other.  Every g below the best b is kept and
@@ -518,8 +520,29 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
                         }
                         k0 = z ? inG : inB;
                         k1 = z ? inB : inG;
-                    } else if (__any_sync(FULL, 2 * P > L)) {
-                        need_rank = true;
+                    } else if (__any_sync(FULL, 2 * P > Lc)) {
+                        // growth past a list size that is not a power of two (P < Lc < 2P):
+                        // keep the Lc smallest of the 2P candidates by (metric, index),
+                        // the candidate index of the u = 1 child being Lc + p (_kernels.py:253-267)
+                        float *um = cg;
+                        int *ui = reinterpret_cast<int *>(cg + 2 * L);
+                        if (act) {
+                            um[pl] = c0;
+                            ui[pl] = pl;
+                            um[P + pl] = c1;
+                            ui[P + pl] = Lc + pl;
+                        }
+                        __syncwarp();
+                        int r0 = 0, r1 = 0;
+                        for (int q = 0; q < 2 * P; ++q) {
+                            const float v = um[q];
+                            const int vi = ui[q];
+                            r0 += v < c0 || (v == c0 && vi < pl);
+                            r1 += v < c1 || (v == c1 && vi < Lc + pl);
+                        }
+                        k0 = act && r0 < Lc;
+                        k1 = act && r1 < Lc;
+                        __syncwarp();
                     }
                     // ---- slot assignment (_kernels.py:271-311) ----
                     const uint32_t freeM = (__ballot_sync(FULL, act && !k0 && !k1) >> gbase) & gmask_lo;

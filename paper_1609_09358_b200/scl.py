@@ -55,10 +55,8 @@ class SclConfig:
             raise ValueError("decision-aid threshold must lie in [0, 1]")
 
     def native(self, virtual_levels: int | None = None, warps_per_cta: int = 0, kernel: int | None = None) -> nat.PcSclCfg:
-        if self.list_size > 32 or self.list_size & (self.list_size - 1):
-            raise ValueError(
-                f"the device list decoder supports L in {{1, 2, 4, 8, 16, 32}}, got {self.list_size}"
-            )
+        if self.list_size > 32:
+            raise ValueError(f"the device list decoder supports list sizes up to 32, got {self.list_size}")
         return nat.PcSclCfg(
             self.list_size,
             int(self.metric_mode == "exact"),
@@ -212,6 +210,9 @@ def scl_decode_batch(
     cfg = cfg or SclConfig()
     if code.N < 2:
         raise ValueError("list decoding needs a block length of at least 2")
+    L = cfg.list_size
+    if L & (L - 1) and code.N < 64:
+        raise ValueError(f"a list size that is not a power of two (L={L}) needs N >= 64 on the device")
     torch = nat.require_device()
     lib = nat.load()
     host = not (hasattr(llrs, "is_cuda") and llrs.is_cuda)

@@ -189,3 +189,29 @@ def test_sc_kernel_matches_list_kernel_at_l1(N, crc, fmode, mmode, da, B):
             os.environ["PC_SCL_KERNEL"] = old
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("N,L,eb,count", [(256, 3, 1.5, 300), (256, 5, 1.0, 300), (1024, 6, 1.5, 200),
+                                          (1024, 12, 1.5, 150), (512, 20, 1.0, 150), (256, 31, 1.5, 120)])
+def test_any_list_size_matches_oracle(N, L, eb, count):
+    """The reference accepts any list size (scl.py:57).  A list size that is
+    not a power of two runs on the next power of two of lanes with L paths;
+    winners, metrics and CRC flags equal the fp64 oracle's (which restates the
+    reference's selection for any L)."""
+    code = CodeConfig(N, N // 2, crc=16)
+    sigma = ebno_to_sigma(eb, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(404, L, f))[1] for f in range(count)])
+    llrs = llrs.astype(np.float32).astype(np.float64)
+    got = scl_decode_batch(llrs, code, SclConfig(L))
+    u, mt, ok = oracle.scl_batch(llrs, code, L)
+    assert np.array_equal(got.u_hat, u)
+    assert np.array_equal(got.crc_ok, ok)
+    assert np.allclose(got.metric, mt, rtol=2e-5, atol=1e-5)
+
+
+def test_list_size_limits():
+    code = CodeConfig(32, 16, crc=None)
+    with pytest.raises(ValueError):
+        SclConfig(33).native()
+    with pytest.raises(ValueError):  # not a power of two and N < 64
+        scl_decode_batch(np.zeros((1, 32)), code, SclConfig(3))
