@@ -240,7 +240,7 @@ def test_scl_workspace_size_query_without_gpu():
     large = lib.pc_scl_workspace_bytes(ctypes.byref(code_struct(4096, 2048)), ctypes.byref(ps.SclConfig(32).native()))
     assert small > 256 and large > 256  # resident warps x windows x 160 B
     bad = ps.SclConfig(32).native()
-    bad.L = 3
+    bad.L = 33  # list sizes 1..32 (any; N >= 64 when not a power of two)
     assert lib.pc_scl_workspace_bytes(ctypes.byref(code_struct(1024, 512)), ctypes.byref(bad)) == -1
     # v2 (N < 32) needs only the counter block
     assert lib.pc_scl_workspace_bytes(ctypes.byref(code_struct(16, 8, 0)), ctypes.byref(ps.SclConfig(4).native())) \
