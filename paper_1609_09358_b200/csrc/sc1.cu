@@ -37,10 +37,16 @@ __host__ __device__ constexpr int pso(int s) { return (1 << (s - 5)) - 1; } // p
 // recomputed from the channel (scl_math.cuh::virt_top) when the descent
 // crosses them (each of levels 9..n-1 is visited 2^(n-1-s) times per frame), so
 // a frame needs 2.5 KB of shared memory at N = 2048 instead of 8.5 KB.
-__host__ __device__ constexpr int top_level(int n) { return n - 1 < 8 ? n - 1 : 8; }
+#ifndef SC1_TOP
+#define SC1_TOP 8
+#endif
+__host__ __device__ constexpr int top_level(int n) { return n - 1 < SC1_TOP ? n - 1 : SC1_TOP; }
 __host__ __device__ inline int frame_words(int N, int n) // levels, partial sums, decisions, leaf LLRs, increments
 {
-    return (2 << top_level(n)) - 32 + 2 * (N / 32) + 96;
+    // a stride of 4 (mod 32) words: the G frames of a warp (32/G lanes each,
+    // consecutive elements) fall in distinct banks (with a multiple of 32 they
+    // all hit the same ones: ncu measured 84% of the shared wavefronts as conflicts)
+    return (((2 << top_level(n)) - 32 + 2 * (N / 32) + 96 + 31) & ~31) + 4;
 }
 __host__ __device__ inline int table_words(int N) { return N + 2 * (N / 32); } // columns, frozen, da
 } // namespace sc1
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
         daS[i] = a.code.da_bits != nullptr ? a.code.da_bits[i] : 0u;
     }
     __syncthreads();
-    const int tp = NV > 0 ? 8 : n - 1; // top stored level
+    const int tp = NV > 0 ? SC1_TOP : n - 1; // top stored level
     float *lv = reinterpret_cast<float *>(smw + table_words(N) + ((threadIdx.x >> 5) * G + grp) * frame_words(N, n));
     uint32_t *ps = reinterpret_cast<uint32_t *>(lv + (2 << tp) - 32);
     uint32_t *ub = ps + NW;
@@ -416,11 +422,12 @@ static int launch_sc1_t(const SclArgs &a, cudaStream_t s)
 template <bool FEX, int G>
 static int launch_sc1_g(const SclArgs &a, cudaStream_t s)
 {
-    switch (a.code.n > 9 ? a.code.n - 9 : 0) { // NV: virtual levels above level 8
+    switch (a.code.n > SC1_TOP + 1 ? a.code.n - SC1_TOP - 1 : 0) { // NV: virtual levels above the top stored level
     case 0: return launch_sc1_t<FEX, G, 0>(a, s);
     case 1: return launch_sc1_t<FEX, G, 1>(a, s);
     case 2: return launch_sc1_t<FEX, G, 2>(a, s);
     case 3: return launch_sc1_t<FEX, G, 3>(a, s);
+    case 4: return launch_sc1_t<FEX, G, 4>(a, s);
     }
     return PC_ERR_UNSUPPORTED;
 }
