@@ -51,6 +51,15 @@ __host__ __device__ inline int frame_words(int N, int n) // levels, partial sums
 __host__ __device__ inline int table_words(int N) { return N + 2 * (N / 32); } // columns, frozen, da
 } // namespace sc1
 
+// Shared words of one warp: its G frames, plus (G = 1) the frame's deferred metric
+// terms and its channel row (the upper levels re-read it; from global memory
+// every read is an L2 round trip on the single warp's critical path).
+template <int G>
+__host__ __device__ inline int sc1_frame_words(int N, int n)
+{
+    return G * sc1::frame_words(N, n) + (G == 1 ? 3 * N + 4 + ((N / 32 + 3) & ~3) : 0);
+}
+
 // One block of 32 leaves from its level-5 LLRs x (K3 v3's leaf code at L = 1):
 // decisions bu, the fp32 metric, the CRC syndrome and the block codeword betaT.
 // SPEC = false: the exact rule at every leaf (decision c1 < c0 of the metric
@@ -219,6 +228,48 @@ __device__ __forceinline__ bool metric_pass(uint32_t fzw, uint32_t daw, uint32_t
     return same;
 }
 
+// The polar transform of a 32-bit word (bit i = position i): [a xor b, b]
+// recursively, the same bit layout as the leaf code's block codeword.  An
+// involution, so it also maps a codeword back to its decisions.
+__device__ __forceinline__ uint32_t polar32(uint32_t v)
+{
+    v ^= (v >> 1) & 0x55555555u;
+    v ^= (v >> 2) & 0x33333333u;
+    v ^= (v >> 4) & 0x0F0F0F0Fu;
+    v ^= (v >> 8) & 0x00FF00FFu;
+    v ^= (v >> 16) & 0x0000FFFFu;
+    return v;
+}
+
+// Leaf LLRs of a 32-leaf block for given decisions u (bit j = leaf j), one
+// leaf per lane: the block's subtree breadth-first, level s holding element
+// (lane & (2^s - 1)) of node (lane >> s); a node's two parent elements sit in
+// lanes lane and lane ^ 2^s.  The g operations take the left sibling's
+// codeword from the partial transforms T_s of u.  Same f / g on the same
+// values as the leaf code, so the LLRs are bit-identical to it whenever u
+// agrees with the decisions before each leaf.
+template <bool FEX>
+__device__ __forceinline__ float leaves32(float xl, uint32_t u, int lane)
+{
+    uint32_t T[5];
+    T[0] = u;
+    T[1] = T[0] ^ ((T[0] >> 1) & 0x55555555u);
+    T[2] = T[1] ^ ((T[1] >> 2) & 0x33333333u);
+    T[3] = T[2] ^ ((T[2] >> 4) & 0x0F0F0F0Fu);
+    T[4] = T[3] ^ ((T[3] >> 8) & 0x00FF00FFu);
+    float v = xl;
+#pragma unroll
+    for (int s = 4; s >= 0; --s) {
+        const int h = 1 << s;
+        const float p = __shfl_xor_sync(0xffffffffu, v, h);
+        if (lane & h) // right child: g with the left sibling's codeword
+            v = scl_g(p, v, (T[s] >> (lane & ~h)) & 1u);
+        else
+            v = scl_f<FEX>(v, p);
+    }
+    return v;
+}
+
 template <bool FEX, int G, int NV>
 __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
 {
@@ -240,11 +291,18 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
     }
     __syncthreads();
     const int tp = NV > 0 ? SC1_TOP : n - 1; // top stored level
-    float *lv = reinterpret_cast<float *>(smw + table_words(N) + ((threadIdx.x >> 5) * G + grp) * frame_words(N, n));
+    float *lv = reinterpret_cast<float *>(smw + table_words(N) + (size_t)(threadIdx.x >> 5) * sc1_frame_words<G>(N, n) +
+                                          grp * frame_words(N, n));
     uint32_t *ps = reinterpret_cast<uint32_t *>(lv + (2 << tp) - 32);
     uint32_t *ub = ps + NW;
     float *lam = reinterpret_cast<float *>(ub + NW); // 32 leaf LLRs of the current block
     float *inc = lam + 32;                            // their metric increments (u = 0, u = 1)
+    // G = 1: the frame's deferred metric terms (chosen / other increment per leaf, confirm bits)
+    float *incS = reinterpret_cast<float *>(smw) + table_words(N) + (size_t)(threadIdx.x >> 5) * sc1_frame_words<G>(N, n) +
+                  frame_words(N, n);
+    float *incO = incS + N + 4;
+    uint32_t *chk = reinterpret_cast<uint32_t *>(incO + N);
+    float *chS = incO + N + ((NW + 3) & ~3); // G = 1: the channel row
     const int total = a.count != nullptr ? *a.count : a.B;
     const int nblk = N >> T;
 
@@ -259,8 +317,24 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
         const bool live = qi < total;
         const int frame = live ? (a.queue != nullptr ? a.queue[qi] : qi) : 0;
         const float *ch = a.llr + (size_t)frame * N;
+        if constexpr (G == 1) {
+            const float4 *g4p = reinterpret_cast<const float4 *>(ch);
+            for (int t = lane; t < N / 4; t += 32)
+                reinterpret_cast<float4 *>(chS)[t] = __ldg(g4p + t);
+            __syncwarp();
+            ch = chS;
+        }
         float metric = 0.0f, m_blk = 0.0f; // m_blk, s_blk: metric and syndrome at the block's start
         uint32_t syn = 0u, s_blk = 0u;
+        // G = 1: pass 0 decides every block by the fixpoint and defers the metric to
+        // one chain over the frame's leaves; if that chain rejects a decision (or a
+        // fixpoint did not settle), pass 1 decodes the frame again with the exact
+        // per-block path.  G > 1: the per-block path only.
+        for (int pass = (G == 1 ? 0 : 1); pass < 2; ++pass) {
+        const bool fast = G == 1 && pass == 0;
+        metric = m_blk = 0.0f;
+        syn = s_blk = 0u;
+        bool settled = true;
         for (int b = 0; b < nblk; ++b) {
             const int i0 = b << T;
             // ---- upper descent: levels start..5, element-parallel over the group ----
@@ -291,7 +365,7 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                 }
                 if (s + 1 == n) { // from the channel (global memory, coalesced)
                     for (int t = pl; t < w; t += GL) {
-                        const float A = __ldg(ch + t), B = __ldg(ch + t + w);
+                        const float A = ch[t], B = ch[t + w];
                         dst[t] = g ? scl_g(A, B, (pw[t >> 5] >> (t & 31)) & 1u) : scl_f<FEX>(A, B);
                     }
                 } else {
@@ -306,8 +380,48 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
             // ---- the block's 32 leaves on the group's first lane, registers only
             // (K3 v3's leaf code at L = 1) ----
             uint32_t betaT = 0, bu = 0;
-            float x[32];
             const uint32_t fzw = frzS[b], daw = daS[b];
+            if (fast) {
+                // One frame per warp (latency form): the block's decisions as the fixpoint
+                // of u = rule(lambda(u)), one leaf per lane.  lambda_j depends on u_0..u_j-1
+                // only, so after round r the first r decisions are final and the fixpoint
+                // (reached in <= 32 rounds, typically 1-3 from the hard-decision guess) is
+                // the sequential decoder's.  The rule here is u = (lambda < 0) at info
+                // leaves; the metric pass below checks it against the exact rule.
+                const float xl = lv[lane];
+                const uint32_t info = ~fzw;
+                uint32_t u = polar32(__ballot_sync(FULL, xl < 0.0f)) & info;
+                float laml = 0.0f;
+                bool conv = false;
+                for (int r = 0; r < 40; ++r) {
+                    laml = leaves32<FEX>(xl, u, lane);
+                    const uint32_t un = __ballot_sync(FULL, laml < 0.0f) & info;
+                    if (un == u) {
+                        conv = true;
+                        break;
+                    }
+                    u = un;
+                }
+                settled &= conv;
+                bu = u;
+                betaT = polar32(u);
+                syn ^= __reduce_xor_sync(FULL, ((u >> lane) & 1u) ? colS[i0 + lane] : 0u);
+                // the leaf's increment for its decision, the other one, and whether the
+                // exact rule must confirm the decision (info leaf decided 1: the rule keeps
+                // u = 1 only if metric + inc1 < metric + inc0; a leaf decided 0 has
+                // inc0 <= inc1 and stays 0)
+                float i0v, i1v;
+                metric_incs(laml, a.metric_exact, i0v, i1v);
+                const bool u1 = (u >> lane) & 1u;
+                incS[i0 + lane] = u1 ? i1v : i0v;
+                incO[i0 + lane] = u1 ? i0v : i1v;
+                const uint32_t ck = __ballot_sync(FULL, u1 && !((daw >> lane) & 1u));
+                if (lane == 0) {
+                    chk[b] = ck;
+                    ub[b] = bu;
+                }
+            } else {
+            float x[32];
             if (pl == 0) { // the decision chain (speculative), leaf LLRs into lam[]
 #pragma unroll
                 for (int t = 0; t < 32; t += 4) {
@@ -339,6 +453,7 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                 s_blk = syn;
                 ub[b] = bu;
             }
+            }
             // ---- block end: fold the block codeword into the stored partial sums ----
             betaT = __shfl_sync(FULL, betaT, grp * GL);
             const int S = T + __ffs(~b) - 1; // level of the node this block completes
@@ -353,6 +468,39 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                 }
             }
             __syncwarp();
+        }
+        if (!fast)
+            break;
+        // the frame's metric: one fp32 chain over the leaves in order (the reference's
+        // order of additions) on lane 0, writing the metric before each leaf over its
+        // chosen increment; then every lane checks its leaves: a leaf the exact rule
+        // must confirm keeps u = 1 only if (metric before) + inc1 < (metric before) + inc0
+        if (lane == 0) {
+            float m = 0.0f;
+            for (int i = 0; i < N; i += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(incS + i);
+                float4 pre;
+                pre.x = m;
+                m += v.x;
+                pre.y = m;
+                m += v.y;
+                pre.z = m;
+                m += v.z;
+                pre.w = m;
+                m += v.w;
+                *reinterpret_cast<float4 *>(incS + i) = pre; // incS[i] := the metric before leaf i
+            }
+            metric = m;
+            incS[N] = m; // (the metric after the last leaf)
+        }
+        __syncwarp();
+        bool ok = settled;
+        for (int i = lane; i < N; i += 32)
+            if ((chk[i >> 5] >> (i & 31)) & 1u)
+                ok &= incS[i + 1] < incS[i] + incO[i];
+        ok = __all_sync(FULL, ok);
+        if (ok)
+            break;
         }
         // ---- outputs (the one path is the winner, scl.py:177-191) ----
         metric = __shfl_sync(FULL, metric, grp * GL);
@@ -397,7 +545,7 @@ static int launch_sc1_t(const SclArgs &a, cudaStream_t s)
     const int N = a.code.N, n = a.code.n;
     int wpc = 4;
     auto bytes = [&](int w) {
-        return ((size_t)sc1::table_words(N) + (size_t)w * G * sc1::frame_words(N, n)) * 4;
+        return ((size_t)sc1::table_words(N) + (size_t)w * sc1_frame_words<G>(N, n)) * 4;
     };
     while (wpc > 1 && bytes(wpc) > 227 * 1024)
         wpc >>= 1;
