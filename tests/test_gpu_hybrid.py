@@ -218,3 +218,27 @@ def test_scl_queue_subset_and_empty_queue():
                 assert np.array_equal(p[f], full.payload_words[f].cpu().numpy())
             else:
                 assert np.all(p[f] == -1)
+
+
+@pytest.mark.parametrize("L", [1, 6])
+def test_hybrid_any_list_size_vs_oracle(L):
+    """The hybrid with a list size that is not a power of two (L = 6: the list
+    decoder keeps 6 paths on 8 lanes) and with L = 1 (the SC kernel on the
+    queue of BP failures): payloads equal the oracle's on every frame both
+    sides route alike."""
+    import torch
+
+    code = CodeConfig(1024, 512, crc=16)
+    sigma = ebno_to_sigma(1.5, code.rate)
+    llrs = np.array([make_frame(code, sigma, frame_rng(2025, L, f))[1] for f in range(800)])
+    llrs = llrs.astype(np.float32).astype(np.float64)
+    pay, prov, iters = oracle.hybrid_batch(llrs, code, i_max=50, L=L)
+    dec = HybridDecoder(code, BpConfig(i_max=50), SclConfig(L), capacity=800, chunk=256)
+    dec.run(torch.from_numpy(llrs.astype(np.float32)).cuda()).sync()
+    r = dec.host_results()
+    got = nat.unpack_bits(r["payload"], code.message_len)
+    flips = np.flatnonzero(~r["converged"] != prov)
+    diff = np.flatnonzero((got != pay).any(axis=1))
+    assert set(diff.tolist()) <= set(flips.tolist())
+    assert np.all(iters[flips] > 20) and flips.size <= 0.02 * len(llrs)
+    assert (~r["converged"]).sum() > 100  # the list decoder ran on a real queue
