@@ -34,6 +34,15 @@
 
 namespace pc {
 
+#ifdef SCL3_STATS
+// development counters (tools/scl3_stats.py): full-list selections, those with an
+// uncertain set, those settled by one swap, those ranked, clones
+static __device__ unsigned long long g_scl3_stats[8];
+#define S3_COUNT(i) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_scl3_stats[i], 1ull); } while (0)
+#else
+#define S3_COUNT(i) do { } while (0)
+#endif
+
 namespace s3 {
 
 
@@ -443,12 +452,15 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
                         const uint32_t bm = gmin_u<L>(act ? bk : FULL);
                         const bool hiG = act && gk >= bm, loB = act && bk <= gm;
                         bool inG = act, inB = false;
+                        S3_COUNT(0);
                         if (__any_sync(FULL, hiG)) {
+                            S3_COUNT(1);
                             const uint32_t gb = (__ballot_sync(FULL, hiG) >> gbase) & gmask_lo;
                             const uint32_t bb = (__ballot_sync(FULL, loB) >> gbase) & gmask_lo;
                             const int h = __popc(gb), l = __popc(bb);
                             // (a group with some g >= min b has h >= 1 and l >= 1)
                             if (__all_sync(FULL, h <= 1 || l <= 1)) {
+                                S3_COUNT(2);
                                 // one swap at most: the worst kept g against the best dropped b
                                 const int gx = gmax_i<L>(act && gk == gm ? gi : -1);
                                 const int bx = gmin_i<L>(act && bk == bm ? bi : 2 * L);
@@ -569,6 +581,7 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
                     if (anydup)
                         __syncwarp();
                     if (__any_sync(FULL, src != lane)) {
+                        S3_COUNT(3);
                         const float pc1 = __shfl_sync(FULL, c1, src);
                         // eager copy of the still-readable register levels: level s+1 while
                         // bit s of j is 0 (the reference's rule at _kernels.py:296-303)
