@@ -48,7 +48,11 @@ __host__ __device__ inline int frame_words(int N, int n) // levels, partial sums
     // all hit the same ones: ncu measured 84% of the shared wavefronts as conflicts)
     return (((2 << top_level(n)) - 32 + 2 * (N / 32) + 96 + 31) & ~31) + 4;
 }
-__host__ __device__ inline int table_words(int N) { return N + 2 * (N / 32); } // columns, frozen, da
+// CTA tables: 32 zero words (the CRC columns of a code without a CRC; the
+// columns themselves are read through L1, in the latency form one per lane,
+// issued before the block's descent), frozen and decision-aided words
+template <int G>
+__host__ __device__ inline int table_words(int N) { return 32 + 2 * (N / 32); }
 } // namespace sc1
 
 // Shared words of one warp: its G frames, plus (G = 1) the frame's deferred metric
@@ -280,25 +284,26 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
     const int N = a.code.N, n = a.code.n, NW = N >> 5;
     const int lane = threadIdx.x & 31, grp = lane / GL, pl = lane % GL;
     uint32_t *colS = smw;
-    uint32_t *frzS = colS + N;
+    uint32_t *frzS = colS + 32;
     uint32_t *daS = frzS + NW;
     const bool use_crc = a.code.crc_width > 0;
     for (int i = threadIdx.x; i < N; i += blockDim.x)
-        colS[i] = use_crc ? a.code.crc_cols[i] : 0u;
+        if (i < 32)
+            colS[i] = 0u;
     for (int i = threadIdx.x; i < NW; i += blockDim.x) {
         frzS[i] = a.code.frozen_bits[i];
         daS[i] = a.code.da_bits != nullptr ? a.code.da_bits[i] : 0u;
     }
     __syncthreads();
     const int tp = NV > 0 ? SC1_TOP : n - 1; // top stored level
-    float *lv = reinterpret_cast<float *>(smw + table_words(N) + (size_t)(threadIdx.x >> 5) * sc1_frame_words<G>(N, n) +
+    float *lv = reinterpret_cast<float *>(smw + table_words<G>(N) + (size_t)(threadIdx.x >> 5) * sc1_frame_words<G>(N, n) +
                                           grp * frame_words(N, n));
     uint32_t *ps = reinterpret_cast<uint32_t *>(lv + (2 << tp) - 32);
     uint32_t *ub = ps + NW;
     float *lam = reinterpret_cast<float *>(ub + NW); // 32 leaf LLRs of the current block
     float *inc = lam + 32;                            // their metric increments (u = 0, u = 1)
     // G = 1: the frame's deferred metric terms (chosen / other increment per leaf, confirm bits)
-    float *incS = reinterpret_cast<float *>(smw) + table_words(N) + (size_t)(threadIdx.x >> 5) * sc1_frame_words<G>(N, n) +
+    float *incS = reinterpret_cast<float *>(smw) + table_words<G>(N) + (size_t)(threadIdx.x >> 5) * sc1_frame_words<G>(N, n) +
                   frame_words(N, n);
     float *incO = incS + N + 4;
     uint32_t *chk = reinterpret_cast<uint32_t *>(incO + N);
@@ -306,11 +311,18 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
     const int total = a.count != nullptr ? *a.count : a.B;
     const int nblk = N >> T;
 
-    for (;;) {
+    // work == nullptr: the launch holds a warp for every G frames (small batches),
+    // so frames go by warp index and no counter has to be reset first
+    const int static_base = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * G;
+    for (int round = 0;; ++round) {
         int base = 0;
-        if (lane == 0)
-            base = atomicAdd(a.work, G);
-        base = __shfl_sync(FULL, base, 0);
+        if (a.work == nullptr) {
+            base = round == 0 ? static_base : total;
+        } else {
+            if (lane == 0)
+                base = atomicAdd(a.work, G);
+            base = __shfl_sync(FULL, base, 0);
+        }
         if (base >= total)
             break;
         const int qi = base + grp;
@@ -337,6 +349,8 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
         bool settled = true;
         for (int b = 0; b < nblk; ++b) {
             const int i0 = b << T;
+            // (latency form: this lane's CRC column of the block, in flight during the descent)
+            const uint32_t colv = G == 1 && use_crc ? __ldg(a.code.crc_cols + i0 + lane) : 0u;
             // ---- upper descent: levels start..5, element-parallel over the group ----
             const int start = (b == 0) ? n - 1 : T + __ffs(b) - 1;
             for (int s = start < tp ? start : tp; s >= T; --s) {
@@ -405,7 +419,7 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                 settled &= conv;
                 bu = u;
                 betaT = polar32(u);
-                syn ^= __reduce_xor_sync(FULL, ((u >> lane) & 1u) ? colS[i0 + lane] : 0u);
+                syn ^= __reduce_xor_sync(FULL, ((u >> lane) & 1u) ? colv : 0u);
                 // the leaf's increment for its decision, the other one, and whether the
                 // exact rule must confirm the decision (info leaf decided 1: the rule keeps
                 // u = 1 only if metric + inc1 < metric + inc0; a leaf decided 0 has
@@ -428,7 +442,8 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                     const float4 v = *reinterpret_cast<const float4 *>(lv + t);
                     x[t] = v.x, x[t + 1] = v.y, x[t + 2] = v.z, x[t + 3] = v.w;
                 }
-                leaf_chain<FEX, true>(x, fzw, daw, colS + i0, a.metric_exact, lam, metric, syn, bu, betaT);
+                leaf_chain<FEX, true>(x, fzw, daw, use_crc ? a.code.crc_cols + i0 : colS, a.metric_exact, lam, metric,
+                                      syn, bu, betaT);
             }
             __syncwarp();
             // the metric increments of the 32 leaves, element-parallel over the group
@@ -447,7 +462,8 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                     // block from its start (metric and syndrome as they were)
                     metric = m_blk;
                     syn = s_blk;
-                    leaf_chain<FEX, false>(x, fzw, daw, colS + i0, a.metric_exact, lam, metric, syn, bu, betaT);
+                    leaf_chain<FEX, false>(x, fzw, daw, use_crc ? a.code.crc_cols + i0 : colS, a.metric_exact, lam,
+                                           metric, syn, bu, betaT);
                 }
                 m_blk = metric;
                 s_blk = syn;
@@ -543,27 +559,42 @@ static int launch_sc1_t(const SclArgs &a, cudaStream_t s)
 {
     auto kern = k_sc1<FEX, G, NV>;
     const int N = a.code.N, n = a.code.n;
-    int wpc = 4;
-    auto bytes = [&](int w) {
-        return ((size_t)sc1::table_words(N) + (size_t)w * sc1_frame_words<G>(N, n)) * 4;
-    };
-    while (wpc > 1 && bytes(wpc) > 227 * 1024)
-        wpc >>= 1;
-    const size_t smem = bytes(wpc);
-    if (smem > 227 * 1024)
+    auto bytes = [&](int w) { return ((size_t)sc1::table_words<G>(N) + (size_t)w * sc1_frame_words<G>(N, n)) * 4; };
+    if (bytes(1) > 227 * 1024)
         return PC_ERR_UNSUPPORTED;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
         return PC_ERR_CUDA;
-    int dev = 0, sms = 0, per_sm = 0;
+    // warps per CTA: the most frames resident per SM (each CTA carries the tables
+    // once; registers allow 16 warps per SM), fewer warps on a tie
+    // (G = 1, the latency form: four warps, so the CTA stages the tables fast)
+    int wpc = 1, best = 0;
+    for (int w = G == 1 ? 4 : 1; w <= 4; ++w) {
+        int per_sm = 0;
+        if (bytes(w) > 227 * 1024 ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * w, bytes(w)) != cudaSuccess)
+            break;
+        if (per_sm * w * G > best) {
+            best = per_sm * w * G;
+            wpc = w;
+        }
+    }
+    cudaGetLastError();
+    if (best == 0)
+        return PC_ERR_UNSUPPORTED;
+    const size_t smem = bytes(wpc);
+    int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpc, smem) != cudaSuccess || per_sm < 1)
-        return PC_ERR_UNSUPPORTED;
-    long long grid = (long long)sms * per_sm;
+    long long grid = (long long)sms * (best / (wpc * G));
     const long long need = ((long long)a.B + (long long)wpc * G - 1) / ((long long)wpc * G);
-    if (grid > need)
-        grid = need;
-    kern<<<(int)grid, 32 * wpc, smem, s>>>(a);
+    SclArgs b = a;
+    if (grid >= need && a.count == nullptr) {
+        grid = need; // one warp per G frames: static assignment, no counter
+        b.work = nullptr;
+    } else if (cudaMemsetAsync(a.work, 0, sizeof(int32_t), s) != cudaSuccess) {
+        return PC_ERR_CUDA;
+    }
+    kern<<<(int)grid, 32 * wpc, smem, s>>>(b);
     return cudaGetLastError() == cudaSuccess ? PC_OK : PC_ERR_CUDA;
 }
 
@@ -589,8 +620,6 @@ int launch_sc1(const SclArgs &a, cudaStream_t s)
 {
     if (a.B == 0)
         return PC_OK;
-    if (cudaMemsetAsync(a.work, 0, sizeof(int32_t), s) != cudaSuccess)
-        return PC_ERR_CUDA;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
