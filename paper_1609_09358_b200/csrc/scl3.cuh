@@ -438,6 +438,7 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
                     const float c0 = act ? metric + inc0 : INFINITY;
                     const float c1 = act ? metric + inc1 : INFINITY;
                     bool k0 = act, k1 = act;
+                    bool trivial = false; // full list, every path keeps its agreeing child
                     if (__any_sync(FULL, P == Lc)) {
                         // ---- selection at a full list: exactly the L best of 2L by (metric, index) ----
                         // (live groups share P; a finished group has P = 0 and takes no part)
@@ -453,7 +454,14 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
                         const bool hiG = act && gk >= bm, loB = act && bk <= gm;
                         bool inG = act, inB = false;
                         S3_COUNT(0);
-                        if (__any_sync(FULL, hiG)) {
+                        // (no g at or above the best b: the L agreeing children are the L best,
+                        // no slot frees or clones -- 77% of the full-list selections, tools/scl3_stats.py)
+                        trivial = !__any_sync(FULL, hiG);
+                        if (trivial && act) {
+                            u = z ? 0u : 1u;
+                            metric = gv;
+                        }
+                        if (!trivial) {
                             S3_COUNT(1);
                             const uint32_t gb = (__ballot_sync(FULL, hiG) >> gbase) & gmask_lo;
                             const uint32_t bb = (__ballot_sync(FULL, loB) >> gbase) & gmask_lo;
@@ -557,6 +565,7 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
                         __syncwarp();
                     }
                     // ---- slot assignment (_kernels.py:271-311) ----
+                    if (!trivial) {
                     const uint32_t freeM = (__ballot_sync(FULL, act && !k0 && !k1) >> gbase) & gmask_lo;
                     const uint32_t dupM = (__ballot_sync(FULL, act && k0 && k1) >> gbase) & gmask_lo;
                     const int nf = __popc(freeM), nd = __popc(dupM);
@@ -628,6 +637,7 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
                         }
                     }
                     P = P == 0 ? 0 : P - nf + nd;
+                    }
                 }
                 // ---- record the decision (non-frozen positions) ----
                 if (!fz) {
