@@ -272,9 +272,10 @@ class HybridDecoder:
             cur.wait_event(h2d[i])
             if i >= 2:  # batch i-2's results (same decoder) have been copied out
                 cur.wait_event(d2h[i - 2])
-            dec.run(self._dbuf[i % NBUF][:B], B)
+            # (join=False: batch i+1, on the twin, starts its BP stage beside this SCL stage)
+            dec.run(self._dbuf[i % NBUF][:B], B, join=False)
             ev = torch.cuda.Event()
-            ev.record(cur)
+            ev.record(dec.s_scl)  # the SCL stage ends after the batch's last BP launch
             done[i] = ev
             pay, conv = self._pinned_out(i, B)
             with torch.cuda.stream(self._s_back):
@@ -287,6 +288,8 @@ class HybridDecoder:
             outs.append((pay, conv))
         self._s_copy.synchronize()
         self._s_back.synchronize()
+        for d in decs:
+            d.join_streams()
         cur.synchronize()
         return [(p.numpy().view(np.uint32), c.numpy().view(np.bool_)) for p, c in outs]
 
