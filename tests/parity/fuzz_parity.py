@@ -82,7 +82,9 @@ SCL_FRAMES = 0
 
 def scl_case(rng, seed):
     code = draw_code(rng)
-    L = int(rng.choice([1, 2, 4, 8, 16, 32]))
+    L = int(rng.choice([1, 2, 3, 4, 6, 8, 12, 16, 20, 32]))  # any list size (N >= 64 if not a power of two)
+    if L & (L - 1) and code.N < 64:
+        L = 1 << (L.bit_length() - 1)
     cfg = SclConfig(L, metric_mode=str(rng.choice(["exact", "approx"])), f_mode=str(rng.choice(["minsum", "exact"])),
                     selector=str(rng.choice(["pseudo", "bitonic"])),
                     da_threshold=float(rng.choice([0.0, 0.0, 0.3])))
