@@ -54,6 +54,7 @@ def lib():
             "oc_bp_decode": (i32, [vp, vp, i32, i32, f64, i32, vp, vp, vp, vp, vp]),
             "oc_bp_g": (f64, [f64, f64, i32, f64]),
             "oc_scl_paths": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, vp, vp]),
+            "oc_set_margin_out": (None, [vp]),
             "oc_scl_decode": (i32, [vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp]),
             "oc_scl_f": (f64, [f64, f64, i32]),
             "oc_metric_inc": (f64, [f64, i32, i32]),
@@ -280,3 +281,16 @@ def cpu_count() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+def scl_min_margin(llr, code, L, da=None, metric_mode="exact", f_mode="minsum", selector="pseudo"):
+    """(gap, metric, leaf): the smallest gap between the worst kept and the best
+    dropped candidate over the frame's list selections (single-threaded; a
+    test diagnostic for fp32 selection ties)."""
+    out = np.array([np.inf, 0.0, -1.0])
+    lib().oc_set_margin_out(_p(out))
+    try:
+        scl_decode(llr, code, L, da=da, metric_mode=metric_mode, f_mode=f_mode, selector=selector)
+    finally:
+        lib().oc_set_margin_out(None)
+    return float(out[0]), float(out[1]), int(out[2])

@@ -274,6 +274,57 @@ __device__ __forceinline__ float leaves32(float xl, uint32_t u, int lane)
     return v;
 }
 
+// The G > 1 form of leaves32: a frame's 32 leaves on its GL = 32/E lanes, E
+// consecutive leaves per lane (element e = lane-in-group * E + k).  Pairs 2^s
+// apart with 2^s < E are registers of one lane; wider ones are lanes
+// 2^s / E apart within the group (shfl.xor).  Same f / g on the same values.
+template <bool FEX, int E>
+__device__ __forceinline__ void leaves_e(const float (&xv)[E], uint32_t u, int pl, float (&v)[E])
+{
+    uint32_t T[5];
+    T[0] = u;
+    T[1] = T[0] ^ ((T[0] >> 1) & 0x55555555u);
+    T[2] = T[1] ^ ((T[1] >> 2) & 0x33333333u);
+    T[3] = T[2] ^ ((T[2] >> 4) & 0x0F0F0F0Fu);
+    T[4] = T[3] ^ ((T[3] >> 8) & 0x00FF00FFu);
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+        v[k] = xv[k];
+#pragma unroll
+    for (int s = 4; s >= 0; --s) {
+        const int h = 1 << s;
+        if (h < E) {
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                if (k & h)
+                    continue;
+                const float a = v[k], b = v[k | h];
+                v[k] = scl_f<FEX>(a, b);
+                v[k | h] = scl_g(a, b, (T[s] >> (pl * E + k)) & 1u);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                const float p = __shfl_xor_sync(0xffffffffu, v[k], h / E);
+                const int e = pl * E + k;
+                v[k] = (e & h) ? scl_g(p, v[k], (T[s] >> (e & ~h)) & 1u) : scl_f<FEX>(v[k], p);
+            }
+        }
+    }
+}
+
+// The 32-bit word of a frame's per-leaf predicate (E leaves per lane, GL lanes from gbase).
+template <int E>
+__device__ __forceinline__ uint32_t gather_bits(uint32_t local, int gbase)
+{
+    constexpr int GL = 32 / E;
+    uint32_t w = 0;
+#pragma unroll
+    for (int q = 0; q < GL; ++q)
+        w |= __shfl_sync(0xffffffffu, local, gbase + q) << (q * E);
+    return w;
+}
+
 template <bool FEX, int G, int NV>
 __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
 {
@@ -435,6 +486,74 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                     ub[b] = bu;
                 }
             } else {
+#ifndef SC1_GFIX
+#define SC1_GFIX 1
+#endif
+#if SC1_GFIX
+            // G > 1: the fixpoint of the latency form, E = G leaves per lane
+            constexpr int E = 32 / GL;
+            float xv[E], lv_[E];
+#pragma unroll
+            for (int k = 0; k < E; ++k)
+                xv[k] = lv[pl * E + k];
+            const uint32_t info = ~fzw;
+            const int gb = grp * GL;
+            uint32_t loc = 0;
+#pragma unroll
+            for (int k = 0; k < E; ++k)
+                loc |= (xv[k] < 0.0f ? 1u : 0u) << k;
+            uint32_t u = polar32(gather_bits<E>(loc, gb)) & info;
+            bool conv = false;
+            for (int r = 0; r < 40; ++r) {
+                leaves_e<FEX, E>(xv, u, pl, lv_);
+                loc = 0;
+#pragma unroll
+                for (int k = 0; k < E; ++k)
+                    loc |= (lv_[k] < 0.0f ? 1u : 0u) << k;
+                const uint32_t un = gather_bits<E>(loc, gb) & info;
+                conv = un == u;
+                u = un;
+                if (__all_sync(FULL, conv))
+                    break;
+            }
+            bu = u;
+            betaT = polar32(u);
+            uint32_t cx = 0;
+#pragma unroll
+            for (int k = 0; k < E; ++k)
+                if (use_crc && ((u >> (pl * E + k)) & 1u))
+                    cx ^= __ldg(a.code.crc_cols + i0 + pl * E + k);
+#pragma unroll
+            for (int off = 1; off < GL; off <<= 1)
+                cx ^= __shfl_xor_sync(FULL, cx, off);
+            syn ^= cx;
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                float i0v, i1v;
+                metric_incs(lv_[k], a.metric_exact, i0v, i1v);
+                inc[2 * (pl * E + k)] = i0v;
+                inc[2 * (pl * E + k) + 1] = i1v;
+            }
+            __syncwarp();
+            if (pl == 0) {
+                if (!conv || !metric_pass(fzw, daw, bu, inc, metric)) {
+                    // exact replay of the block from its start state
+                    float x[32];
+#pragma unroll
+                    for (int t = 0; t < 32; t += 4) {
+                        const float4 v = *reinterpret_cast<const float4 *>(lv + t);
+                        x[t] = v.x, x[t + 1] = v.y, x[t + 2] = v.z, x[t + 3] = v.w;
+                    }
+                    metric = m_blk;
+                    syn = s_blk;
+                    leaf_chain<FEX, false>(x, fzw, daw, use_crc ? a.code.crc_cols + i0 : colS, a.metric_exact, lam,
+                                           metric, syn, bu, betaT);
+                }
+                m_blk = metric;
+                s_blk = syn;
+                ub[b] = bu;
+            }
+#else
             float x[32];
             if (pl == 0) { // the decision chain (speculative), leaf LLRs into lam[]
 #pragma unroll
@@ -469,6 +588,7 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                 s_blk = syn;
                 ub[b] = bu;
             }
+#endif
             }
             // ---- block end: fold the block codeword into the stored partial sums ----
             betaT = __shfl_sync(FULL, betaT, grp * GL);

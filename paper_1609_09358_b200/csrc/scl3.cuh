@@ -456,7 +456,10 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
                         S3_COUNT(0);
                         // (no g at or above the best b: the L agreeing children are the L best,
                         // no slot frees or clones -- 77% of the full-list selections, tools/scl3_stats.py)
-                        trivial = !__any_sync(FULL, hiG);
+#ifndef SCL3_TRIVIAL
+#define SCL3_TRIVIAL 1
+#endif
+                        trivial = SCL3_TRIVIAL && !__any_sync(FULL, hiG);
                         if (trivial && act) {
                             u = z ? 0u : 1u;
                             metric = gv;

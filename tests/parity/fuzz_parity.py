@@ -6,7 +6,8 @@ a batch size and decoder knobs, then checks
 * SCL (all knobs, DA masks): winners, CRC flags bit-identical to the oracle,
   except frames whose reference winner passes an info position with an fp64
   leaf LLR below fp32 resolution (1e-5, or 4 ulps of the fp32 path metric:
-  `precision_limited`);
+  `precision_limited`) or whose reference list selection kept and dropped
+  candidates closer than an fp32 metric can resolve (`selection_limited`);
 * BP (crc / reencode / none stop): flags, iterations and u_hat identical on
   all but certified near-tie frames (a small fraction; reported).
 
@@ -76,6 +77,17 @@ def precision_limited(llr, code, u_ref, exact_f, metric_ref=0.0):
     return bool(np.abs(leaves[np.asarray(code.info_positions)]).min() < tol)
 
 
+def selection_limited(llr, code, L, da, cfg):
+    """A list selection of the reference had its worst kept and best dropped
+    candidates closer than the worst-case rounding of an fp32 metric summed
+    over that many leaves (0.5 ulp per addition): the fp32 device cannot
+    resolve which one the list keeps, so the lists (and possibly the winner)
+    part there."""
+    gap, metric, leaf = oracle.scl_min_margin(llr, code, L, da=da, metric_mode=cfg.metric_mode, f_mode=cfg.f_mode,
+                                              selector=cfg.selector)
+    return leaf >= 0 and gap < 0.5 * (leaf + 1) * float(np.spacing(np.float32(abs(metric))))
+
+
 SCL_CERTIFIED = 0
 SCL_FRAMES = 0
 
@@ -100,7 +112,8 @@ def scl_case(rng, seed):
         ref = oracle.scl_decode(llrs[f], code, L, da=da, metric_mode=cfg.metric_mode, f_mode=cfg.f_mode,
                                 selector=cfg.selector)
         if not (np.array_equal(got.u_hat[f], ref["u_hat"]) and bool(got.crc_ok[f]) == ref["crc_ok"]):
-            if precision_limited(llrs[f], code, ref["u_hat"], cfg.f_mode == "exact", ref["metric"]):
+            if precision_limited(llrs[f], code, ref["u_hat"], cfg.f_mode == "exact", ref["metric"]) or \
+                    selection_limited(llrs[f], code, L, da, cfg):
                 SCL_CERTIFIED += 1
             else:
                 bad.append(f)
