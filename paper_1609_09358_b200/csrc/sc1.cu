@@ -21,7 +21,7 @@
 //   * the code tables (CRC syndrome columns, frozen and decision-aided words)
 //     are staged once per CTA in shared memory, so a leaf's column read is not
 //     a global-memory round trip on the decision chain.
-// G = 1 is the latency form (one frame per warp, small batches); G = 4 the
+// G = 1 is the latency form (one frame per warp, small batches); G = 8 or 4 the
 // throughput form.  Shared memory per frame: levels 5..n-1 (N - 32 floats),
 // partial sums N/32 words, decisions N/32 words.
 #include "args.cuh"
@@ -274,57 +274,6 @@ __device__ __forceinline__ float leaves32(float xl, uint32_t u, int lane)
     return v;
 }
 
-// The G > 1 form of leaves32: a frame's 32 leaves on its GL = 32/E lanes, E
-// consecutive leaves per lane (element e = lane-in-group * E + k).  Pairs 2^s
-// apart with 2^s < E are registers of one lane; wider ones are lanes
-// 2^s / E apart within the group (shfl.xor).  Same f / g on the same values.
-template <bool FEX, int E>
-__device__ __forceinline__ void leaves_e(const float (&xv)[E], uint32_t u, int pl, float (&v)[E])
-{
-    uint32_t T[5];
-    T[0] = u;
-    T[1] = T[0] ^ ((T[0] >> 1) & 0x55555555u);
-    T[2] = T[1] ^ ((T[1] >> 2) & 0x33333333u);
-    T[3] = T[2] ^ ((T[2] >> 4) & 0x0F0F0F0Fu);
-    T[4] = T[3] ^ ((T[3] >> 8) & 0x00FF00FFu);
-#pragma unroll
-    for (int k = 0; k < E; ++k)
-        v[k] = xv[k];
-#pragma unroll
-    for (int s = 4; s >= 0; --s) {
-        const int h = 1 << s;
-        if (h < E) {
-#pragma unroll
-            for (int k = 0; k < E; ++k) {
-                if (k & h)
-                    continue;
-                const float a = v[k], b = v[k | h];
-                v[k] = scl_f<FEX>(a, b);
-                v[k | h] = scl_g(a, b, (T[s] >> (pl * E + k)) & 1u);
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < E; ++k) {
-                const float p = __shfl_xor_sync(0xffffffffu, v[k], h / E);
-                const int e = pl * E + k;
-                v[k] = (e & h) ? scl_g(p, v[k], (T[s] >> (e & ~h)) & 1u) : scl_f<FEX>(v[k], p);
-            }
-        }
-    }
-}
-
-// The 32-bit word of a frame's per-leaf predicate (E leaves per lane, GL lanes from gbase).
-template <int E>
-__device__ __forceinline__ uint32_t gather_bits(uint32_t local, int gbase)
-{
-    constexpr int GL = 32 / E;
-    uint32_t w = 0;
-#pragma unroll
-    for (int q = 0; q < GL; ++q)
-        w |= __shfl_sync(0xffffffffu, local, gbase + q) << (q * E);
-    return w;
-}
-
 template <bool FEX, int G, int NV>
 __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
 {
@@ -486,74 +435,6 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                     ub[b] = bu;
                 }
             } else {
-#ifndef SC1_GFIX
-#define SC1_GFIX 1
-#endif
-#if SC1_GFIX
-            // G > 1: the fixpoint of the latency form, E = G leaves per lane
-            constexpr int E = 32 / GL;
-            float xv[E], lv_[E];
-#pragma unroll
-            for (int k = 0; k < E; ++k)
-                xv[k] = lv[pl * E + k];
-            const uint32_t info = ~fzw;
-            const int gb = grp * GL;
-            uint32_t loc = 0;
-#pragma unroll
-            for (int k = 0; k < E; ++k)
-                loc |= (xv[k] < 0.0f ? 1u : 0u) << k;
-            uint32_t u = polar32(gather_bits<E>(loc, gb)) & info;
-            bool conv = false;
-            for (int r = 0; r < 40; ++r) {
-                leaves_e<FEX, E>(xv, u, pl, lv_);
-                loc = 0;
-#pragma unroll
-                for (int k = 0; k < E; ++k)
-                    loc |= (lv_[k] < 0.0f ? 1u : 0u) << k;
-                const uint32_t un = gather_bits<E>(loc, gb) & info;
-                conv = un == u;
-                u = un;
-                if (__all_sync(FULL, conv))
-                    break;
-            }
-            bu = u;
-            betaT = polar32(u);
-            uint32_t cx = 0;
-#pragma unroll
-            for (int k = 0; k < E; ++k)
-                if (use_crc && ((u >> (pl * E + k)) & 1u))
-                    cx ^= __ldg(a.code.crc_cols + i0 + pl * E + k);
-#pragma unroll
-            for (int off = 1; off < GL; off <<= 1)
-                cx ^= __shfl_xor_sync(FULL, cx, off);
-            syn ^= cx;
-#pragma unroll
-            for (int k = 0; k < E; ++k) {
-                float i0v, i1v;
-                metric_incs(lv_[k], a.metric_exact, i0v, i1v);
-                inc[2 * (pl * E + k)] = i0v;
-                inc[2 * (pl * E + k) + 1] = i1v;
-            }
-            __syncwarp();
-            if (pl == 0) {
-                if (!conv || !metric_pass(fzw, daw, bu, inc, metric)) {
-                    // exact replay of the block from its start state
-                    float x[32];
-#pragma unroll
-                    for (int t = 0; t < 32; t += 4) {
-                        const float4 v = *reinterpret_cast<const float4 *>(lv + t);
-                        x[t] = v.x, x[t + 1] = v.y, x[t + 2] = v.z, x[t + 3] = v.w;
-                    }
-                    metric = m_blk;
-                    syn = s_blk;
-                    leaf_chain<FEX, false>(x, fzw, daw, use_crc ? a.code.crc_cols + i0 : colS, a.metric_exact, lam,
-                                           metric, syn, bu, betaT);
-                }
-                m_blk = metric;
-                s_blk = syn;
-                ub[b] = bu;
-            }
-#else
             float x[32];
             if (pl == 0) { // the decision chain (speculative), leaf LLRs into lam[]
 #pragma unroll
@@ -588,7 +469,6 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                 s_blk = syn;
                 ub[b] = bu;
             }
-#endif
             }
             // ---- block end: fold the block codeword into the stored partial sums ----
             betaT = __shfl_sync(FULL, betaT, grp * GL);
@@ -675,7 +555,7 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
 bool sc1_eligible(const SclArgs &a) { return a.code.n >= 6 && a.code.n <= 12; }
 
 template <bool FEX, int G, int NV>
-static int launch_sc1_t(const SclArgs &a, cudaStream_t s)
+static int launch_sc1_t(const SclArgs &a, cudaStream_t s, long long *capacity = nullptr)
 {
     auto kern = k_sc1<FEX, G, NV>;
     const int N = a.code.N, n = a.code.n;
@@ -705,6 +585,10 @@ static int launch_sc1_t(const SclArgs &a, cudaStream_t s)
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (capacity != nullptr) { // (a query: frames resident at once, no launch)
+        *capacity = (long long)sms * best;
+        return PC_OK;
+    }
     long long grid = (long long)sms * (best / (wpc * G));
     const long long need = ((long long)a.B + (long long)wpc * G - 1) / ((long long)wpc * G);
     SclArgs b = a;
@@ -719,23 +603,34 @@ static int launch_sc1_t(const SclArgs &a, cudaStream_t s)
 }
 
 template <bool FEX, int G>
-static int launch_sc1_g(const SclArgs &a, cudaStream_t s)
+static int launch_sc1_g(const SclArgs &a, cudaStream_t s, long long *capacity = nullptr)
 {
     switch (a.code.n > SC1_TOP + 1 ? a.code.n - SC1_TOP - 1 : 0) { // NV: virtual levels above the top stored level
-    case 0: return launch_sc1_t<FEX, G, 0>(a, s);
-    case 1: return launch_sc1_t<FEX, G, 1>(a, s);
-    case 2: return launch_sc1_t<FEX, G, 2>(a, s);
-    case 3: return launch_sc1_t<FEX, G, 3>(a, s);
-    case 4: return launch_sc1_t<FEX, G, 4>(a, s);
+    case 0: return launch_sc1_t<FEX, G, 0>(a, s, capacity);
+    case 1: return launch_sc1_t<FEX, G, 1>(a, s, capacity);
+    case 2: return launch_sc1_t<FEX, G, 2>(a, s, capacity);
+    case 3: return launch_sc1_t<FEX, G, 3>(a, s, capacity);
+    case 4: return launch_sc1_t<FEX, G, 4>(a, s, capacity);
     }
     return PC_ERR_UNSUPPORTED;
 }
 
-// G = 1 (latency form, one frame per warp) while the batch fits one frame per
-// resident warp, else SC1_G frames per warp (throughput form).
-#ifndef SC1_G
-#define SC1_G 8
-#endif
+template <bool FEX>
+static int launch_sc1_f(const SclArgs &a, cudaStream_t s, int sms)
+{
+    // G = 1 (latency form, one frame per warp) while the batch fits one frame per
+    // resident warp; else 8 frames per warp when the batch then fits one wave of
+    // resident frames, 4 when it does not (measured at N = 2048: 4 frames per warp
+    // run each wave faster, 8 hold more frames at once: 10^4 frames 16.1 vs 12.9
+    // Mframes/s, 32768 frames 14.7 vs 19.1)
+    if (a.B <= sms * 8)
+        return launch_sc1_g<FEX, 1>(a, s);
+    long long cap8 = 0;
+    if (launch_sc1_g<FEX, 8>(a, s, &cap8) == PC_OK && a.B <= cap8)
+        return launch_sc1_g<FEX, 8>(a, s);
+    return launch_sc1_g<FEX, 4>(a, s);
+}
+
 int launch_sc1(const SclArgs &a, cudaStream_t s)
 {
     if (a.B == 0)
@@ -743,10 +638,7 @@ int launch_sc1(const SclArgs &a, cudaStream_t s)
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const bool small = a.B <= sms * 8;
-    if (small)
-        return a.f_exact ? launch_sc1_g<true, 1>(a, s) : launch_sc1_g<false, 1>(a, s);
-    return a.f_exact ? launch_sc1_g<true, SC1_G>(a, s) : launch_sc1_g<false, SC1_G>(a, s);
+    return a.f_exact ? launch_sc1_f<true>(a, s, sms) : launch_sc1_f<false>(a, s, sms);
 }
 
 } // namespace pc
