@@ -91,6 +91,10 @@ __device__ __forceinline__ void b_c(const float (&v)[8], float (&o)[8], float *x
 
 } // namespace b3
 
+#ifndef PC_BP3_FUSE
+#define PC_BP3_FUSE 1
+#endif
+
 __host__ __device__ constexpr int bp3_smem_floats(int logn)
 {
     // R[8..n-1], L[8..n], N bytes of decisions, warp scratch
@@ -110,6 +114,10 @@ __global__ void __launch_bounds__((1 << LOGN) / 8) k_bp3(const BpArgs a)
     constexpr int NW = N / 32;
     constexpr int NWARP = TPF / 32;
     constexpr int PPT = N / 2 / TPF;   // shared-memory PEs per thread (single boundaries)
+    // fused turn of the sweeps at the top pair (n-1, n) when the shared
+    // boundaries 9..n pair up evenly (N = 1024, 4096)
+    constexpr bool FUSE = LOGN >= BW + 2 && (LOGN - BW) % 2 == 0 && PC_BP3_FUSE;
+    constexpr int RTOP = FUSE ? LOGN - 2 : LOGN - 1; // highest R row of the R sweep proper
     static_assert(LOGN >= 8 && LOGN <= 12, "bp3 geometry: 256..4096 nodes, 8 per thread");
 
     extern __shared__ __align__(16) float sm[];
@@ -196,14 +204,15 @@ __global__ void __launch_bounds__((1 << LOGN) / 8) k_bp3(const BpArgs a)
                 Rs[wb + xc(lane, r)] = R8[r];
         }
         __syncthreads();
-        // shared-memory boundaries in radix-4 pairs (j, j+1), as in k_bp2
+        // shared-memory boundaries in radix-4 pairs (j, j+1), as in k_bp2; with
+        // FUSE the top pair (n-1, n) is left to the fused turn below
 #pragma unroll
-        for (int j = BW + 1; j <= LOGN - 1; j += 2) {
+        for (int j = BW + 1; j <= RTOP; j += 2) {
             const int h = 1 << (j - 1);
             const float *Rp = Rs + (j - 1 - BW) * N;
             float *Rd = Rs + (j - BW) * N;
             const float *Lj = Ls + (j - BW) * N;
-            if (j + 1 <= LOGN - 1) {
+            if (j + 1 <= RTOP) {
                 float *Rd2 = Rs + (j + 1 - BW) * N;
                 const float *Lj2 = Ls + (j + 1 - BW) * N;
 #pragma unroll
@@ -246,9 +255,66 @@ __global__ void __launch_bounds__((1 << LOGN) / 8) k_bp3(const BpArgs a)
             }
             __syncthreads();
         }
+        if constexpr (FUSE) {
+            // The turn of the sweep: R[n-1] (boundary n-1), then L[n-1] (boundary
+            // n) and L[n-2] (boundary n-1), group by group.  A radix-4 group
+            // {g, g+h, g+2h, g+3h} (h = N/4) is closed under boundaries n-1 and n,
+            // so R[n-1] stays in registers and no barrier separates the sweeps.
+            // The operations and their inputs are those of the separate R single
+            // and L pair passes (bit-identical).
+            constexpr int j = LOGN - 1;
+            constexpr int h = 1 << (j - 1);
+            const float *Rp = Rs + (j - 1 - BW) * N;
+            float *Rj = Rs + (j - BW) * N;
+            float *Lm = Ls + (j - BW) * N;
+            const float *Lt = Ls + (j + 1 - BW) * N;
+            float *Ld = Ls + (j - 1 - BW) * N;
+            const bool keep_r = RE || a.soft_x != nullptr; // R[n-1] is read after the loop
+#pragma unroll 1
+            for (int q = 0; q < Q / 4; ++q) {
+                const int n0 = tid + q * TPF, n1 = n0 + h, n2 = n0 + 2 * h, n3 = n0 + 3 * h;
+                float o[4], m[4], rp[4];
+                rp[0] = Rp[n0];
+                rp[1] = Rp[n1];
+                rp[2] = Rp[n2];
+                rp[3] = Rp[n3];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) { // R[n-1] from R[n-2] and L[n-1] (old)
+                    const float l1 = Lm[e ? n2 : n0], l2 = Lm[e ? n3 : n1];
+                    bp_pe2<GMODE, true>(rp[2 * e], bp_comb<GMODE>(l2, rp[2 * e + 1]), l1, rp[2 * e + 1], lim, o[2 * e],
+                                        o[2 * e + 1]);
+                }
+                if (keep_r) {
+                    Rj[n0] = o[0];
+                    Rj[n1] = o[1];
+                    Rj[n2] = o[2];
+                    Rj[n3] = o[3];
+                }
+#pragma unroll
+                for (int e = 0; e < 2; ++e) { // L[n-1] from the channel row and R[n-1]
+                    const int i1 = e ? n1 : n0, i2 = i1 + 2 * h;
+                    const float l1 = Lt[i1], l2 = Lt[i2];
+                    bp_pe2<GMODE, false>(l1, bp_comb<GMODE>(l2, o[e + 2]), o[e], l2, lim, m[e], m[e + 2]);
+                }
+                Lm[n0] = m[0];
+                Lm[n1] = m[1];
+                Lm[n2] = m[2];
+                Lm[n3] = m[3];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) { // L[n-2] from L[n-1] and R[n-2]
+                    const int i1 = e ? n2 : n0, i2 = i1 + h;
+                    float o1, o2;
+                    bp_pe2<GMODE, false>(m[2 * e], bp_comb<GMODE>(m[2 * e + 1], rp[2 * e + 1]), rp[2 * e],
+                                         m[2 * e + 1], lim, o1, o2);
+                    Ld[i1] = o1;
+                    Ld[i2] = o2;
+                }
+            }
+            __syncthreads();
+        }
         // ================= L sweep =================
 #pragma unroll
-        for (int jt = LOGN; jt >= BW + 1; jt -= 2) {
+        for (int jt = FUSE ? LOGN - 2 : LOGN; jt >= BW + 1; jt -= 2) {
             if (jt - 1 >= BW + 1) {
                 const int j = jt - 1;
                 const int h = 1 << (j - 1);
