@@ -51,9 +51,9 @@ def mufu_per_alg_g(n: int) -> float:
 
 
 def k1_tpf(N: int) -> int:
-    """K1's default threads per frame for the likelihood-ratio form (bp2.cu
-    bp2_default_tpf: Q = 8 nodes per thread, at least one warp)."""
-    return max(32, N // 8)
+    """K1's default threads per frame for the likelihood-ratio form: Q = 8
+    nodes per thread (bp3.cu from N = 256, bp3h.cu at N = 128: a half-warp)."""
+    return N // 8
 
 
 def _clock_mhz(ck):
@@ -70,7 +70,10 @@ def k1_kernel_label(N: int) -> str:
     if N >= 256:
         return (f"k_bp3<{n},0> (BP, likelihood-ratio arithmetic, {N // 8} threads/frame, warp-local boundaries in "
                 "three register layouts joined by shared-memory transposes)")
-    return f"k_bp2<{n},{k1_tpf(N)},0> (BP, likelihood-ratio arithmetic, lane-pair shuffles, one warp per frame)"
+    if N == 128:
+        return ("k_bp3h<0> (BP, likelihood-ratio arithmetic, a frame per half-warp, 7 boundaries in three register "
+                "layouts joined by shared-memory transposes)")
+    return f"k_bp2<{n},{max(32, N // 8)},0> (BP, likelihood-ratio arithmetic, lane-pair shuffles, one warp per frame)"
 
 
 def k1_roofline(torch, dev, N: int, g_total: float, k1_s: float, ck, frames_per_launch=None) -> dict:

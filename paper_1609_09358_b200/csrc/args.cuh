@@ -49,6 +49,8 @@ bool bp2_eligible(const BpArgs &a, int g_mode, int tpf);
 int launch_bp2(const BpArgs &a, int g_mode, int tpf, cudaStream_t s);
 bool bp3_eligible(const BpArgs &a, int g_mode, int tpf);
 int launch_bp3(const BpArgs &a, int g_mode, cudaStream_t s);
+bool bp3h_eligible(const BpArgs &a, int g_mode, int tpf);
+int launch_bp3h(const BpArgs &a, int g_mode, cudaStream_t s);
 int launch_bp_iterate(float *l, float *r, int B, int n, int g_mode, float lim, cudaStream_t s);
 int scl_prepare(SclArgs &a, int nv_req);
 int launch_scl(const SclArgs &a, int L, int wpc, cudaStream_t s);

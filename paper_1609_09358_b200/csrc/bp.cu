@@ -360,8 +360,13 @@ int launch_bp_decode(const BpArgs &a, int g_mode, int tpf, int kernel, cudaStrea
     if (g_mode == 2 || g_mode == 3) // exact g, per-g / round-1 log-domain forms: K1 v2 only
         return launch_bp2(a, g_mode, tpf, s);
     // kernel: 0 auto (v3 where eligible, else v2, else v1), 1 v1, 2 v2, 3 v3
-    if (kernel == 3)
+    if (kernel == 3) {
+        if (bp3h_eligible(a, g_mode, tpf))
+            return launch_bp3h(a, g_mode, s);
         return bp3_eligible(a, g_mode, tpf) ? launch_bp3(a, g_mode, s) : PC_ERR_UNSUPPORTED;
+    }
+    if (kernel == 0 && bp3h_eligible(a, g_mode, tpf))
+        return launch_bp3h(a, g_mode, s);
     if (kernel == 0 && bp3_eligible(a, g_mode, tpf))
         return launch_bp3(a, g_mode, s);
     if (kernel == 2 && !bp2_eligible(a, g_mode, tpf))

@@ -393,13 +393,17 @@ def test_soft_x_matches_oracle(N):
         assert mixed_err(res.soft_u, ref["soft_u"]) <= 1e-3
 
 
-@pytest.mark.parametrize("N,mode,g_mode", [(256, "crc", "exact"), (1024, "crc", "exact"), (1024, "reencode", "exact"),
-                                           (2048, "none", "exact"), (4096, "crc", "exact"), (512, "crc", "min")])
-def test_layout_kernel_matches_shuffle_kernel(N, mode, g_mode):
+@pytest.mark.parametrize("N,mode,g_mode,pers", [(256, "crc", "exact", False), (1024, "crc", "exact", False),
+                                                (1024, "reencode", "exact", False), (2048, "none", "exact", False),
+                                                (4096, "crc", "exact", False), (512, "crc", "min", False),
+                                                (128, "crc", "exact", False), (128, "crc", "exact", True),
+                                                (128, "none", "min", True), (256, "crc", "exact", True)])
+def test_layout_kernel_matches_shuffle_kernel(N, mode, g_mode, pers):
     """K1 v3 (bp3.cu: warp-local boundaries in three register layouts joined by
-    shared-memory transposes) and K1 v2 (bp2.cu: lane-pair shuffles) at the
-    same 8 nodes per thread evaluate every PE with the same arithmetic:
-    bit-identical u_hat, soft_u, soft_x, iterations and flags."""
+    shared-memory transposes; bp3h.cu at N = 128: a frame per half-warp) and
+    K1 v2 (bp2.cu: lane-pair shuffles) evaluate every PE with the same
+    arithmetic: bit-identical u_hat, soft_u, soft_x, iterations and flags,
+    with and without the persistent frame counter."""
     import ctypes
 
     import torch
@@ -412,8 +416,13 @@ def test_layout_kernel_matches_shuffle_kernel(N, mode, g_mode):
                                   dtype=np.float32)).cuda()
     dc = nat.device_code(code)
     outs = []
+    work = torch.zeros(1, dtype=torch.int32, device="cuda")
     for kern in (2, 3):
-        cfg = BpConfig(i_max=30, stop_mode=mode, g_mode=g_mode).native(threads_per_frame=N // 8, kernel=kern)
+        # (K1 v2 runs one warp per frame at N = 128: 4 nodes per thread)
+        tpf = N // 8 if kern == 3 or N >= 256 else 32
+        cfg = BpConfig(i_max=30, stop_mode=mode, g_mode=g_mode).native(threads_per_frame=tpf, kernel=kern)
+        if pers and kern == 3:
+            cfg.work = work.data_ptr()
         u = torch.zeros((B, N // 32), dtype=torch.int32, device="cuda")
         su = torch.zeros((B, N), device="cuda")
         sx = torch.zeros((B, N), device="cuda")
@@ -428,7 +437,7 @@ def test_layout_kernel_matches_shuffle_kernel(N, mode, g_mode):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("N,mode", [(256, "crc"), (1024, "reencode"), (1024, "crc"), (2048, "none")])
+@pytest.mark.parametrize("N,mode", [(128, "crc"), (256, "crc"), (1024, "reencode"), (1024, "crc"), (2048, "none")])
 def test_all_bp_kernels_bit_identical(N, mode):
     """With the likelihood-ratio arithmetic every BP kernel evaluates a PE with
     the same bp_math.cuh::bp_pe2 on the same message values, so the
@@ -447,7 +456,8 @@ def test_all_bp_kernels_bit_identical(N, mode):
     dc = nat.device_code(code)
     outs = []
     for kern in (1, 2, 3):
-        cfg = BpConfig(i_max=30, stop_mode=mode).native(threads_per_frame=N // 8 if kern > 1 else 0, kernel=kern)
+        tpf = 0 if kern == 1 else (N // 8 if kern == 3 or N >= 256 else 32)
+        cfg = BpConfig(i_max=30, stop_mode=mode).native(threads_per_frame=tpf, kernel=kern)
         u = torch.zeros((B, N // 32), dtype=torch.int32, device="cuda")
         su = torch.zeros((B, N), device="cuda")
         it = torch.zeros(B, dtype=torch.int32, device="cuda")
