@@ -2,7 +2,7 @@
 // seven boundaries in registers (sm_100a).
 //
 // The N = 128 member of the layout family of bp3.cu (same recursion, stop
-// rules and outputs as k_bp2, reference bp.py:120-217, and the same per-PE
+// rules -- CRC, re-encode, none -- and outputs as k_bp2, reference bp.py:120-217, and the same per-PE
 // arithmetic bp_math.cuh::bp_pe2, so bit-identical to k_bp2<7, ...>).  A frame
 // is 16 threads of 8 nodes.  With h = lane >> 4 the half-warp and l = lane & 15
 // its lane, the nodes of a thread are, by layout:
@@ -94,10 +94,10 @@ __device__ __forceinline__ void b_c(const float (&v)[8], float (&o)[8], float *x
 constexpr int BP3H_WARPS = 4; // warps per CTA (8 frames)
 
 #ifndef PC_BP3H_MINB
-#define PC_BP3H_MINB 1
+#define PC_BP3H_MINB 4 // 128 registers: 4 CTAs per SM (measured best; 5 and 6 were slower)
 #endif
 
-template <int GMODE, bool PERS>
+template <int GMODE, bool PERS, bool RE>
 __global__ void __launch_bounds__(32 * BP3H_WARPS, PC_BP3H_MINB) k_bp3h(const BpArgs a)
 {
     using namespace b3h;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(32 * BP3H_WARPS, PC_BP3H_MINB) k_bp3h(const Bp
 #pragma unroll
     for (int r = 0; r < Q; ++r) {
         pri[r] = ((fw >> r) & 1u) ? bp_prior<GMODE>(lim) : bp_zero<GMODE>();
-        col[r] = a.stop_mode == 0 ? __ldg(a.code.crc_cols + base + r) : 0u;
+        col[r] = !RE && a.stop_mode == 0 ? __ldg(a.code.crc_cols + base + r) : 0u;
     }
 
     int f;
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(32 * BP3H_WARPS, PC_BP3H_MINB) k_bp3h(const Bp
         }
         // ================= stop rule (CRC; stop_mode 2 runs i_max iterations) =================
         bool stop = false;
-        if (a.stop_mode == 0) {
+        if (!RE && a.stop_mode == 0) {
             uint32_t syn = 0;
 #pragma unroll
             for (int r = 0; r < Q; ++r)
@@ -196,6 +196,37 @@ __global__ void __launch_bounds__(32 * BP3H_WARPS, PC_BP3H_MINB) k_bp3h(const Bp
             for (int s = 8; s >= 1; s >>= 1)
                 syn ^= __shfl_xor_sync(hm, syn, s, 16);
             stop = (syn == a.code.crc_offset);
+        }
+        if constexpr (RE) {
+            // re-encode stop (bp.py:187), as in k_bp3: x_hat = hard(L[7] + R[7]) with
+            // R[7] from boundary 7 of the R sweep (layout C, through the half's
+            // decision bytes into layout A), against the polar transform of the
+            // thread's 8 decisions: in registers, then across the half's lanes
+            float R7[Q];
+            stage<GMODE, true, 4>(R6c, Lch, R7, lim);
+            __syncwarp(hm);
+#pragma unroll
+            for (int r = 0; r < Q; ++r)
+                ub[xc(l, r)] = bp_neg<GMODE>(bp_comb<GMODE>(Lch[r], R7[r]));
+            uint32_t v = 0;
+#pragma unroll
+            for (int r = 0; r < Q; ++r)
+                v |= (bp_neg<GMODE>(su[r]) ? 1u : 0u) << r;
+#pragma unroll
+            for (int hh = 1; hh < Q; hh <<= 1)
+                v ^= (v >> hh) & (hh == 1 ? 0x55u : (hh == 2 ? 0x33u : 0x0Fu));
+#pragma unroll
+            for (int s = 1; s < 16; s <<= 1) {
+                const uint32_t pv = __shfl_xor_sync(hm, v, s, 16);
+                if (!(l & s))
+                    v ^= pv;
+            }
+            __syncwarp(hm);
+            uint32_t xh = 0;
+#pragma unroll
+            for (int r = 0; r < Q; ++r)
+                xh |= (uint32_t)ub[base + r] << r;
+            stop = !__any_sync(hm, v != xh);
         }
         if (!stop && it < a.i_max)
             continue;
@@ -261,14 +292,15 @@ __global__ void __launch_bounds__(32 * BP3H_WARPS, PC_BP3H_MINB) k_bp3h(const Bp
 
 bool bp3h_eligible(const BpArgs &a, int g_mode, int tpf)
 {
-    return a.code.n == 7 && (g_mode == 0 || g_mode == 1) && (tpf == 0 || tpf == 16) && a.stop_mode != 1;
+    return a.code.n == 7 && (g_mode == 0 || g_mode == 1) && (tpf == 0 || tpf == 16);
 }
 
 template <int GMODE>
 static int launch_bp3h_t(const BpArgs &a, cudaStream_t s)
 {
-    const bool pers = a.work != nullptr;
-    auto kern = pers ? k_bp3h<GMODE, true> : k_bp3h<GMODE, false>;
+    const bool pers = a.work != nullptr, re = a.stop_mode == 1;
+    auto kern = pers ? (re ? k_bp3h<GMODE, true, true> : k_bp3h<GMODE, true, false>)
+                     : (re ? k_bp3h<GMODE, false, true> : k_bp3h<GMODE, false, false>);
     const int per_cta = 2 * BP3H_WARPS;
     long long grid = ((long long)a.B + per_cta - 1) / per_cta;
     if (pers) {

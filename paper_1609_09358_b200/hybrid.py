@@ -405,6 +405,16 @@ class HybridDecoder:
         self.torch.cuda.current_stream(self.device).synchronize()
         return self
 
+    def warm(self):
+        """One all-zero frame through the pipeline (K1, K2 and K3 are all
+        launched; K3 reads its frame count on the device): the one-time costs
+        of a decoder -- lazy loading of its
+        kernels' modules, first-launch attribute calls, the caching allocator --
+        are paid here, not by the first batch a caller times."""
+        torch = self.torch
+        z = torch.zeros((1, self.code.N), dtype=torch.float32, device=self.device)
+        self.run(z, 1).sync()
+
     def host_results(self):
         """Copy per-frame results of the last run to numpy (after sync)."""
         B = self._B
@@ -455,6 +465,7 @@ def hybrid_decode_batch(
         raise ValueError(f"expected {code.N} channel LLRs per job, got {llr_host.shape[1]}")
     if decoder is None:
         dec = HybridDecoder(code, bp_cfg, scl_cfg, capacity=B, chunk=bp_batch_size)
+        dec.warm()
     else:
         dec = decoder
         if dec.code is not code or dec.capacity < B or dec.chunk != bp_batch_size:
