@@ -453,6 +453,38 @@ __global__ void __launch_bounds__((1 << LOGN) / 8) k_bp3(const BpArgs a)
             for (int r = 0; r < Q; ++r)
                 xh |= (uint32_t)ub[base + r] << r;
             stop = !__syncthreads_or(x != xh);
+        } else if constexpr (RE) {
+            // N = 256 (one warp): R[8] = boundary 8 of the R sweep from R[7] (layout C
+            // registers, pairs (r, r + 2)) and the channel row; x_hat through the
+            // decision bytes into layout A, against the transform of u_hat
+            float Lc[Q], R8[Q];
+#pragma unroll
+            for (int r = 0; r < Q; ++r)
+                Lc[r] = Lch[xc(lane, r)];
+            stage<GMODE, true, 2>(R7, Lc, R8, lim);
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < Q; ++r)
+                ub[xc(lane, r)] = bp_neg<GMODE>(bp_comb<GMODE>(Lc[r], R8[r]));
+            uint32_t v = 0;
+#pragma unroll
+            for (int r = 0; r < Q; ++r)
+                v |= (bp_neg<GMODE>(su[r]) ? 1u : 0u) << r;
+#pragma unroll
+            for (int h = 1; h < Q; h <<= 1)
+                v ^= (v >> h) & (h == 1 ? 0x55u : (h == 2 ? 0x33u : 0x0Fu));
+#pragma unroll
+            for (int s = 1; s < 32; s <<= 1) {
+                const uint32_t pv = __shfl_xor_sync(0xffffffffu, v, s);
+                if (!(lane & s))
+                    v ^= pv;
+            }
+            __syncwarp();
+            uint32_t xh = 0;
+#pragma unroll
+            for (int r = 0; r < Q; ++r)
+                xh |= (uint32_t)ub[base + r] << r;
+            stop = !__any_sync(0xffffffffu, v != xh);
         }
         if (stop || it >= a.i_max)
             break;
@@ -530,14 +562,14 @@ static int launch_bp3_t(const BpArgs &a, cudaStream_t s)
 {
     constexpr int TPF = (1 << LOGN) / 8;
     auto kern = k_bp3<LOGN, GMODE, false, false>;
-    if constexpr (LOGN >= 9)
-        if (a.stop_mode == 1)
-            kern = k_bp3<LOGN, GMODE, true, false>;
+    if (a.stop_mode == 1)
+        kern = k_bp3<LOGN, GMODE, true, false>;
     constexpr bool PERS_OK = TPF <= 64;
-    const bool pers = PERS_OK && a.work != nullptr && a.stop_mode != 1;
+    // (the re-encode stop runs persistent only at N = 256, one warp per frame)
+    const bool pers = PERS_OK && a.work != nullptr && (a.stop_mode != 1 || LOGN == 8);
     if constexpr (PERS_OK)
         if (pers)
-            kern = k_bp3<LOGN, GMODE, false, true>;
+            kern = a.stop_mode == 1 ? k_bp3<LOGN, GMODE, true, true> : k_bp3<LOGN, GMODE, false, true>;
     const size_t smem = (size_t)bp3_smem_floats(LOGN) * sizeof(float);
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -559,8 +591,7 @@ static int launch_bp3_t(const BpArgs &a, cudaStream_t s)
 }
 
 // K1 v3 covers N = 256 .. 4096 at 8 nodes per thread (threads_per_frame N/8),
-// g_mode 0 (likelihood ratios) and 1 (min-sum), every stop rule (re-encode:
-// N >= 512, where R[n-1] is a shared row).
+// g_mode 0 (likelihood ratios) and 1 (min-sum), every stop rule.
 bool bp3_eligible(const BpArgs &a, int g_mode, int tpf)
 {
     const int n = a.code.n;
@@ -568,7 +599,7 @@ bool bp3_eligible(const BpArgs &a, int g_mode, int tpf)
         return false;
     if (tpf > 0 && tpf != a.code.N / 8)
         return false;
-    return a.stop_mode != 1 || n >= 9;
+    return true;
 }
 
 int launch_bp3(const BpArgs &a, int g_mode, cudaStream_t s)

@@ -398,7 +398,8 @@ def test_soft_x_matches_oracle(N):
                                                 (4096, "crc", "exact", False), (512, "crc", "min", False),
                                                 (128, "crc", "exact", False), (128, "crc", "exact", True),
                                                 (128, "none", "min", True), (128, "reencode", "exact", True),
-                                                (128, "reencode", "min", False), (256, "crc", "exact", True)])
+                                                (128, "reencode", "min", False), (256, "crc", "exact", True),
+                                                (256, "reencode", "exact", True), (256, "reencode", "min", False)])
 def test_layout_kernel_matches_shuffle_kernel(N, mode, g_mode, pers):
     """K1 v3 (bp3.cu: warp-local boundaries in three register layouts joined by
     shared-memory transposes; bp3h.cu at N = 128: a frame per half-warp) and
@@ -419,8 +420,8 @@ def test_layout_kernel_matches_shuffle_kernel(N, mode, g_mode, pers):
     outs = []
     work = torch.zeros(1, dtype=torch.int32, device="cuda")
     for kern in (2, 3):
-        # (K1 v2 runs one warp per frame at N = 128: 4 nodes per thread; 2 for the re-encode stop)
-        tpf = N // 8 if kern == 3 or N >= 256 else (64 if mode == "reencode" else 32)
+        # (K1 v2 needs at least a warp per frame, 64 threads for the re-encode stop)
+        tpf = N // 8 if kern == 3 else max(N // 8, 64 if mode == "reencode" else 32)
         cfg = BpConfig(i_max=30, stop_mode=mode, g_mode=g_mode).native(threads_per_frame=tpf, kernel=kern)
         if pers and kern == 3:
             cfg.work = work.data_ptr()
@@ -438,8 +439,8 @@ def test_layout_kernel_matches_shuffle_kernel(N, mode, g_mode, pers):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("N,mode", [(128, "crc"), (128, "reencode"), (256, "crc"), (1024, "reencode"), (1024, "crc"),
-                                    (2048, "none")])
+@pytest.mark.parametrize("N,mode", [(128, "crc"), (128, "reencode"), (256, "crc"), (256, "reencode"), (1024, "reencode"),
+                                    (1024, "crc"), (2048, "none")])
 def test_all_bp_kernels_bit_identical(N, mode):
     """With the likelihood-ratio arithmetic every BP kernel evaluates a PE with
     the same bp_math.cuh::bp_pe2 on the same message values, so the
@@ -458,7 +459,7 @@ def test_all_bp_kernels_bit_identical(N, mode):
     dc = nat.device_code(code)
     outs = []
     for kern in (1, 2, 3):
-        tpf = 0 if kern == 1 else (N // 8 if kern == 3 or N >= 256 else (64 if mode == "reencode" else 32))
+        tpf = 0 if kern == 1 else (N // 8 if kern == 3 else max(N // 8, 64 if mode == "reencode" else 32))
         cfg = BpConfig(i_max=30, stop_mode=mode).native(threads_per_frame=tpf, kernel=kern)
         u = torch.zeros((B, N // 32), dtype=torch.int32, device="cuda")
         su = torch.zeros((B, N), device="cuda")
