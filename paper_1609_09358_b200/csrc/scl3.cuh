@@ -355,6 +355,12 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
             const uint32_t bmask = BL == 32 ? 0xffffffffu : ((1u << (BL & 31)) - 1u);
             const uint32_t fzw = (__ldg(frzg + (i0 >> 5)) >> (i0 & 31)) & bmask;
             const uint32_t daw = damg != nullptr ? (__ldg(damg + (i0 >> 5)) >> (i0 & 31)) & bmask : 0u;
+            // the block's CRC syndrome columns, one per lane (a leaf takes its own by a
+            // shuffle instead of a load on its decision chain)
+#ifndef SCL3_COLB
+#define SCL3_COLB 1
+#endif
+            const uint32_t colb = (SCL3_COLB && use_crc) ? __ldg(colg + i0 + (lane & (BL - 1))) : 0u;
 
             // ================= the block's leaves, registers only =================
             static_assert(T >= 3 && T <= 5, "the leaf code below is written for 8- to 32-leaf blocks");
@@ -419,7 +425,7 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
                 const bool act = pl < P;
                 uint32_t col = 0u;
                 if (!fz && use_crc)
-                    col = __ldg(colg + i);
+                    col = SCL3_COLB ? __shfl_sync(FULL, colb, j) : __ldg(colg + i);
                 float inc0, inc1;
                 metric_incs(lam, a.metric_exact, inc0, inc1);
                 uint32_t u = 0u;
