@@ -481,8 +481,9 @@ def latency_operating_points(torch, code, llr, dev):
     """p50 frame latency under the reference's semantic (a frame's latency runs
     from its BP batch's start to its final decision, hybrid.py:56-66, sim.py:199)
     at small batches: chunks of 32 frames (the reference's bp_batch_size) and
-    1024 frames over 4096 frames per point, and one frame alone on the GPU
-    (64 single-frame runs per point).  Untimed for the headline value."""
+    1024 frames over 4096 frames per point (the chunks' list decoding on up
+    to 8 concurrent SCL streams), and one frame alone on the GPU (64
+    single-frame runs per point).  Untimed for the headline value."""
     from paper_1609_09358_b200 import BpConfig, HybridDecoder, SclConfig
 
     out = []
@@ -500,7 +501,8 @@ def latency_operating_points(torch, code, llr, dev):
             done = np.where(r["converged"], r["t_bp"], r["t_scl"])
             lat = (done - r["stamps"][c, 0]) * 1e-6
             out.append({"ebno_db": EBNO[p], "chunk": ch, "frames": NF, "p50_ms": float(np.median(lat)),
-                        "p99_ms": float(np.percentile(lat, 99)), "gbps_wall": NF * code.message_len / wall / 1e9})
+                        "p99_ms": float(np.percentile(lat, 99)), "gbps_wall": NF * code.message_len / wall / 1e9,
+                        "scl_streams": len(d.s_scls)})
     d1 = HybridDecoder(code, BpConfig(i_max=IMAX), SclConfig(LIST), capacity=1, chunk=1, device=dev)
     for p in pts:
         lat = []

@@ -142,7 +142,8 @@ class HybridDecoder:
     """
 
     def __init__(self, code: CodeConfig, bp_cfg: BpConfig | None = None, scl_cfg: SclConfig | None = None,
-                 capacity: int = 1 << 16, chunk: int | None = None, overlap: bool = True, device=None):
+                 capacity: int = 1 << 16, chunk: int | None = None, overlap: bool = True, device=None,
+                 scl_streams: int | None = None):
         if code.crc is None:
             raise ValueError("hybrid decoding needs a CRC to detect draft failures")
         torch = nat.require_device()
@@ -175,16 +176,26 @@ class HybridDecoder:
         self.counts = torch.zeros(self.nchunks_max, dtype=torch.int32, **z)
         # stamps per chunk: [start, bp_end, scl_start, scl_end]
         self.stamps = torch.zeros((self.nchunks_max, 4), dtype=torch.int64, **z)
-        # this decoder's own K3 workspace (all its chunks' SCL launches are ordered
-        # on one stream) and K1 frame counter (persistent K1 at small N)
-        self.scl_ws = self.dc_scl.new_scl_workspace(self.nscl)
+        # SCL streams (the reference's SCL workers, hybrid.py:153-231): chunk c's
+        # K2 + K3 run on stream c mod S with that stream's own K3 workspace, so
+        # the list decoding of small chunks (bp_batch_size = 32: a few failures,
+        # one warp each) overlaps instead of queueing one chunk behind the other
+        # (default: one per chunk of a full batch, at most 8; 1 without overlap)
+        if scl_streams is None:
+            scl_streams = min(8, self.nchunks_max) if overlap else 1
+        if scl_streams < 1 or (scl_streams > 1 and not overlap):
+            raise ValueError("scl_streams must be >= 1 (and 1 without overlap)")
+        self.scl_wss = [self.dc_scl.new_scl_workspace(self.nscl) for _ in range(scl_streams)]
+        self.scl_ws = self.scl_wss[0]
         self.bp_work = torch.empty(1, dtype=torch.int32, **z)
         self.nbp.work = self.bp_work.data_ptr()
         self.s_bp = torch.cuda.Stream(device=dev)
         # The list decoder's persistent warps get the higher stream priority, so
         # they take SM slots as soon as K1 CTAs (one frame each) retire and the
         # two kernels share the GPU instead of running back to back.
-        self.s_scl = torch.cuda.Stream(device=dev, priority=-1) if overlap else self.s_bp
+        self.s_scls = ([torch.cuda.Stream(device=dev, priority=-1) for _ in range(scl_streams)] if overlap
+                       else [self.s_bp])
+        self.s_scl = self.s_scls[0]  # joins the others at the end of run()
         self.kernel_events = None  # set to [] to time every K1 launch with CUDA events on the BP stream
         self.scl_events = None  # set to [] to time every K2 + K3 pair with CUDA events on the SCL stream
         self.launches_per_chunk = 7  # 4 stamp kernels + K1 + K2 + K3 (memset nodes not counted)
@@ -259,7 +270,8 @@ class HybridDecoder:
         # the copy stream while batch i+1 decodes.
         if getattr(self, "_twin", None) is None:
             self._twin = HybridDecoder(self.code, self.bp_cfg, self.scl_cfg, capacity=self.capacity,
-                                       chunk=self.chunk, overlap=self.overlap, device=self.device)
+                                       chunk=self.chunk, overlap=self.overlap, device=self.device,
+                                       scl_streams=len(self.s_scls))
         decs = (self, self._twin)
         d2h = [None] * len(batches)
         for i in range(min(NBUF - 1, len(batches))):
@@ -336,16 +348,20 @@ class HybridDecoder:
         lib, chk = self.lib, nat.check
         cur = torch.cuda.current_stream(self.device)
         self.s_bp.wait_stream(cur)
-        self.s_scl.wait_stream(cur)
+        for s_ in self.s_scls:
+            s_.wait_stream(cur)
         # this decoder's buffers (payload, flags, queue) are reused: the BP stage of
         # this batch waits for the previous batch's SCL stage when it was not joined
+        # (s_scl has joined the other SCL streams at the end of the previous run)
         self.s_bp.wait_stream(self.s_scl)
         bp_ref, scl_ref = ctypes.byref(self.nbp), ctypes.byref(self.nscl)
         base_llr = llr.data_ptr()
         self._events = []
+        nss = len(self.s_scls)
         for c, b0 in enumerate(range(0, B, self.chunk)):
             nb = min(self.chunk, B - b0)
-            sb, ss = self._st(self.s_bp), self._st(self.s_scl)
+            s_scl = self.s_scls[c % nss]
+            sb, ss = self._st(self.s_bp), self._st(s_scl)
             st = self.stamps[c]
             chk(lib.pc_stamp(st.data_ptr(), sb), "pc_stamp")
             if self.kernel_events is not None:
@@ -367,12 +383,12 @@ class HybridDecoder:
             if self.overlap:
                 ev = torch.cuda.Event()
                 ev.record(self.s_bp)
-                self.s_scl.wait_event(ev)
+                s_scl.wait_event(ev)
                 self._events.append(ev)
             chk(lib.pc_stamp(st.data_ptr() + 16, ss), "pc_stamp")
             if self.scl_events is not None:
                 e2 = torch.cuda.Event(enable_timing=True)
-                e2.record(self.s_scl)
+                e2.record(s_scl)
             q = self.queue.data_ptr() + 4 * b0
             cnt = self.counts.data_ptr() + 4 * c
             chk(lib.pc_compact(self.conv.data_ptr() + b0, nb, q, cnt, None, ss), "pc_compact")
@@ -380,15 +396,17 @@ class HybridDecoder:
                 lib.pc_scl_decode(
                     base_llr + 4 * N * b0, nb, q, cnt, self.dc_scl.ref, scl_ref, None,
                     self.payload.data_ptr() + 4 * self.MW * b0, None, None, None,
-                    self.t_scl.data_ptr() + 8 * b0, self.scl_ws.data_ptr(), ss,
+                    self.t_scl.data_ptr() + 8 * b0, self.scl_wss[c % nss].data_ptr(), ss,
                 ),
                 "pc_scl_decode",
             )
             if self.scl_events is not None:
                 e3 = torch.cuda.Event(enable_timing=True)
-                e3.record(self.s_scl)
+                e3.record(s_scl)
                 self.scl_events.append((e2, e3))
             chk(lib.pc_stamp(st.data_ptr() + 24, ss), "pc_stamp")
+        for s_ in self.s_scls[1:]:
+            self.s_scl.wait_stream(s_)
         self._B = B
         if join:
             self.join_streams()
@@ -430,6 +448,24 @@ class HybridDecoder:
         )
 
 
+def _busy(start, end) -> float:
+    """Seconds covered by the union of the [start, end) globaltimer intervals (ns):
+    the service time of a stage whose chunks may run concurrently (several SCL
+    streams); equal to the sum of the intervals when they do not overlap."""
+    iv = sorted(zip((int(a) for a in start), (int(b) for b in end)))
+    tot, cur_a, cur_b = 0, None, None
+    for a, b in iv:
+        if cur_b is None or a > cur_b:
+            if cur_b is not None:
+                tot += cur_b - cur_a
+            cur_a, cur_b = a, b
+        else:
+            cur_b = max(cur_b, b)
+    if cur_b is not None:
+        tot += cur_b - cur_a
+    return tot * 1e-9
+
+
 def hybrid_decode_batch(
     jobs: list[FrameJob],
     code: CodeConfig,
@@ -444,7 +480,9 @@ def hybrid_decode_batch(
     """Decode jobs through the device pipeline; jobs are completed in place.
 
     ``bp_batch_size`` is the chunk that shares one BP service interval, as in
-    the reference; ``n_scl_workers`` and ``buffer_capacity`` are validated for
+    the reference; ``n_scl_workers`` is the number of SCL streams (at most 8):
+    the list decoding of that many chunks runs concurrently, as the
+    reference's SCL worker threads do; ``buffer_capacity`` is validated for
     API compatibility (the device queue of a chunk always holds all of its
     failures, so it can neither drop nor block).  ``decoder`` reuses a
     ``HybridDecoder`` of the same code across calls (a sweep point's chunks);
@@ -464,7 +502,9 @@ def hybrid_decode_batch(
     if llr_host.shape[1] != code.N:
         raise ValueError(f"expected {code.N} channel LLRs per job, got {llr_host.shape[1]}")
     if decoder is None:
-        dec = HybridDecoder(code, bp_cfg, scl_cfg, capacity=B, chunk=bp_batch_size)
+        # the reference's SCL workers map to SCL streams (concurrent K3 launches)
+        dec = HybridDecoder(code, bp_cfg, scl_cfg, capacity=B, chunk=bp_batch_size,
+                            scl_streams=min(n_scl_workers, 8, (B + bp_batch_size - 1) // bp_batch_size))
         dec.warm()
     else:
         dec = decoder
@@ -490,8 +530,8 @@ def hybrid_decode_batch(
     m = code.message_len
     bits = nat.unpack_bits(r["payload"], m)
     st = r["stamps"]
-    bp_busy = float(np.sum(st[:, 1] - st[:, 0])) * 1e-9
-    scl_busy = float(np.sum(st[:, 3] - st[:, 2])) * 1e-9
+    bp_busy = _busy(st[:, 0], st[:, 1])
+    scl_busy = _busy(st[:, 2], st[:, 3])  # the SCL streams' union: time any of them is busy
     for b, job in enumerate(jobs):
         c = b // bp_batch_size
         job.t_enqueue = job.t_bp_start = float(h(st[c, 0]))

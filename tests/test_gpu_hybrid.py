@@ -168,7 +168,8 @@ def test_n4096_hybrid_vs_oracle():
 
 def test_results_do_not_depend_on_chunking():
     """Per-frame outputs are independent of the chunk size (ragged last chunk,
-    per-chunk queues and counters) and of the stream overlap."""
+    per-chunk queues and counters), of the stream overlap and of the number
+    of SCL streams (concurrent K3 launches on their own workspaces)."""
     import torch
 
     code = CodeConfig(1024, 512, crc=16)
@@ -176,8 +177,10 @@ def test_results_do_not_depend_on_chunking():
     llrs = np.array([make_frame(code, sigma, frame_rng(77, 0, f))[1] for f in range(1000)])
     x = torch.from_numpy(llrs.astype(np.float32)).cuda()
     ref = None
-    for chunk, overlap in ((1000, True), (333, True), (100, False), (1, True)):
-        dec = HybridDecoder(code, BpConfig(i_max=50), SclConfig(32), capacity=1000, chunk=chunk, overlap=overlap)
+    for chunk, overlap, ns in ((1000, True, None), (333, True, None), (100, False, None), (1, True, None),
+                               (32, True, 1), (32, True, 3), (32, True, 8)):
+        dec = HybridDecoder(code, BpConfig(i_max=50), SclConfig(32), capacity=1000, chunk=chunk, overlap=overlap,
+                            scl_streams=ns)
         dec.run(x).sync()
         r = dec.host_results()
         assert r["counts"].sum() == (~r["converged"]).sum()

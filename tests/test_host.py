@@ -260,3 +260,16 @@ def test_c_abi_refuses_unsealed_code_without_gpu():
     assert lib.pc_scl_decode(16, 1, None, None, ctypes.byref(code), ctypes.byref(scfg), None, None, None, None,
                              None, None, 16, None) == -1
     assert lib.pc_encode(16, 1, ctypes.byref(code), 16, None) == -1
+
+
+def test_stage_busy_time_is_the_union_of_intervals():
+    """hybrid._busy: a stage's service time with concurrent chunks (several SCL
+    streams) is the measure of the union of their [start, end) intervals."""
+    from paper_1609_09358_b200.hybrid import _busy
+
+    assert _busy([], []) == 0.0
+    assert _busy([0], [10]) == pytest.approx(10e-9)
+    assert _busy([0, 5, 20], [10, 12, 25]) == pytest.approx(17e-9)  # overlap merged
+    assert _busy([20, 0], [30, 10]) == pytest.approx(20e-9)  # disjoint: the sum
+    big = 1_760_000_000_000_000_000  # globaltimer-sized int64 stamps keep ns resolution
+    assert _busy([big, big + 3], [big + 5, big + 7]) == pytest.approx(7e-9)

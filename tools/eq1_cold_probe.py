@@ -16,7 +16,7 @@ for rep in range(3):
         for f in range(768):
             m, llr = make_frame(code, sigma, frame_rng(800_000 + point, point, f))
             jobs.append(FrameJob(frame_id=f, llrs=llr, true_message=m))
-        st = hybrid_decode_batch(jobs, code, BpConfig(i_max=50), SclConfig(8), bp_batch_size=32, n_scl_workers=2)
+        st = hybrid_decode_batch(jobs, code, BpConfig(i_max=50), SclConfig(8), bp_batch_size=32, n_scl_workers=int(sys.argv[1]) if len(sys.argv) > 1 else 2)
         gap = abs(st.t_hyb_theo_bps - st.throughput_bps) / st.t_hyb_theo_bps
         print(f"rep {rep} {eb} dB gamma={st.gamma_bp_fer:.3f} model={st.t_hyb_theo_bps / 1e6:.1f} Mbps "
               f"measured={st.throughput_bps / 1e6:.1f} Mbps gap={100 * gap:.1f}%", flush=True)
