@@ -320,7 +320,7 @@ class HybridDecoder:
     def _st(self, s) -> int:
         return int(s.cuda_stream)
 
-    def run(self, llr, B: int | None = None, join: bool = True):
+    def run(self, llr, B: int | None = None, join: bool = True, graph: bool = False):
         """Enqueue the pipeline for ``llr[:B]`` (CUDA float32).  Returns immediately;
         call ``sync()`` (or read results) afterwards.
 
@@ -329,7 +329,16 @@ class HybridDecoder:
         batch can then start its BP stage while this batch is still in its SCL
         stage (the paper's Fig. 2 overlap across batches).  This decoder's own
         next batch still starts its BP stage only after this batch's SCL stage
-        (its buffers are reused); call ``join_streams()`` before reading results."""
+        (its buffers are reused); call ``join_streams()`` before reading results.
+
+        ``graph=True`` replays a CUDA graph of the whole pipeline (every chunk's
+        stamps, K1, K2 and K3 on their streams) captured on the first call for
+        this input buffer and batch size: one launch instead of seven per
+        chunk from Python, for loops over small chunks that reuse one input
+        buffer.  The first call runs eagerly and captures; the graph's work is
+        ordered on the caller's stream (``join`` is implied)."""
+        if graph:
+            return self._run_graph(llr, B)
         torch = self.torch
         N = self.code.N
         if not (hasattr(llr, "is_cuda") and llr.is_cuda):
@@ -410,6 +419,31 @@ class HybridDecoder:
         self._B = B
         if join:
             self.join_streams()
+        return self
+
+    def _run_graph(self, llr, B):
+        torch = self.torch
+        if self.kernel_events is not None or self.scl_events is not None:
+            raise ValueError("graph=True does not record per-kernel timing events")
+        B = int(llr.shape[0] if B is None else B)
+        key = (llr.data_ptr(), B, tuple(llr.shape))
+        graphs = getattr(self, "_graphs", None)
+        if graphs is None:
+            graphs = self._graphs = {}
+        g = graphs.get(key)
+        if g is None:
+            self.run(llr, B)  # eager (validates, loads modules, first results)
+            cur = torch.cuda.current_stream(self.device)
+            side = torch.cuda.Stream(device=self.device)
+            side.wait_stream(cur)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                self.run(llr, B)  # enqueued on the BP / SCL streams, which join the capture
+            cur.wait_stream(side)
+            graphs[key] = g
+            return self
+        g.replay()
+        self._B = B
         return self
 
     def join_streams(self):
