@@ -203,9 +203,12 @@ except Exception:
     PORT_OVER_REF = float("nan")
 
 
-def cpu_hybrid_sample(frames_per_point: int, threads: int):
+def cpu_hybrid_sample(frames_per_point: int, threads: int, keep: dict | None = None):
     """The oracle port (oracle/oracle.c, fp64, the reference's algorithm) on the
-    host cores over a bounded sample of the same sweep; returns (Gbit/s, info)."""
+    host cores over a bounded sample of the same sweep; returns (Gbit/s, busy
+    seconds).  The frames are host PCG64 frames with fp32-rounded LLRs (what the
+    device decodes); with ``keep`` the oracle's payloads and provenance per point
+    are stored there for the parity sample."""
     import oracle
     from paper_1609_09358_b200 import CodeConfig
     from paper_1609_09358_b200.channel import ebno_to_sigma, frame_rng, make_frame
@@ -217,14 +220,47 @@ def cpu_hybrid_sample(frames_per_point: int, threads: int):
         key = (p, frames_per_point)
         if key not in _CPU_FRAMES:  # host PCG64 frames, generated once per (point, size)
             sigma = ebno_to_sigma(eb, code.rate)
-            _CPU_FRAMES[key] = np.array([make_frame(code, sigma, frame_rng(SEED, p, f))[1]
-                                         for f in range(frames_per_point)])
-        llrs = _CPU_FRAMES[key]
+            fr = [make_frame(code, sigma, frame_rng(SEED, p, f)) for f in range(frames_per_point)]
+            _CPU_FRAMES[key] = (np.array([f[0] for f in fr]),
+                                np.array([f[1] for f in fr]).astype(np.float32).astype(np.float64))
+        msgs, llrs = _CPU_FRAMES[key]
         t0 = time.perf_counter()
-        oracle.hybrid_batch(llrs, code, i_max=IMAX, L=LIST, nthreads=threads)
+        pay, prov, _ = oracle.hybrid_batch(llrs, code, i_max=IMAX, L=LIST, nthreads=threads)
         busy += time.perf_counter() - t0
         bits += frames_per_point * code.message_len
+        if keep is not None:
+            keep[p] = (msgs, llrs, pay, prov)
     return bits / busy / 1e9, busy
+
+
+def parity_sample(torch, dev, keep: dict) -> dict:
+    """The cpu_baseline sample's frames decoded by the device pipeline beside
+    the oracle's results on the same fp32 LLRs: identical payloads, BP/SCL
+    provenance flips (fp32 vs fp64 near-ties in BP) and the
+    frame errors of both (whose equality in distribution is the parity
+    criterion, tests/parity/fer_parity*.py)."""
+    from paper_1609_09358_b200 import BpConfig, CodeConfig, HybridDecoder, SclConfig
+    from paper_1609_09358_b200 import _native as nat
+
+    code = CodeConfig(N, K, crc=16)
+    m = code.message_len
+    n = max(v[1].shape[0] for v in keep.values())
+    d = HybridDecoder(code, BpConfig(i_max=IMAX), SclConfig(LIST), capacity=n, device=dev)
+    tot = same = flips = fe_dev = fe_ref = 0
+    for p in sorted(keep):
+        msgs, llrs, pay, prov = keep[p]
+        x = torch.from_numpy(llrs.astype(np.float32)).to(dev)
+        r = d.run(x).sync().host_results()
+        got = nat.unpack_bits(r["payload"], m)
+        tot += len(msgs)
+        same += int(np.all(got == pay, axis=1).sum())
+        flips += int(((~r["converged"]) != prov.astype(bool)).sum())
+        fe_dev += int(np.any(got != msgs, axis=1).sum())
+        fe_ref += int(np.any(pay != msgs, axis=1).sum())
+    return {"frames": tot, "payload_identical": same, "provenance_flips": flips, "frame_errors_device": fe_dev,
+            "frame_errors_oracle": fe_ref,
+            "note": "the cpu_baseline frames (host PCG64, fp32-rounded LLRs) through the device pipeline vs the "
+                    "fp64 oracle port of the reference algorithm"}
 
 
 def c3_config(frames: int, chunk: int, world: int) -> dict:
@@ -435,13 +471,15 @@ def run_gpu(args):
     h2d = B * N * 4 * len(EBNO)
     d2h = B * (MW * 4 + 1) * len(EBNO)
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and not args.no_cpu:
         import oracle
 
         threads = oracle.cpu_count()
         fpp = args.cpu_frames or max(2048, 128 * threads)  # ~10 s of oracle work on 16 threads
-        v, busy = cpu_hybrid_sample(fpp, threads)
+        keep = {}
+        v, busy = cpu_hybrid_sample(fpp, threads, keep)
+        parity = parity_sample(torch, dev, keep)
         cpu = {"value": v, "unit": "Gbit/s", "cores": threads, "kind": "port",
                "sample": f"{fpp} frames per Eb/N0 point x {len(EBNO)} points, {busy:.1f} s of CPU wall "
                          f"(fp64 oracle port of the reference algorithm, all host threads)"}
@@ -468,6 +506,7 @@ def run_gpu(args):
             "k3": k3,
             "overlapped": overlapped,
             "cpu_baseline": cpu,
+            "parity_sample": parity,
             "e2e": {"value": e2e_val, "unit": "Gbit/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": args.steps * len(EBNO) * ((B + dec.chunk - 1) // dec.chunk) * dec.launches_per_chunk,
             "clocks": ck,

@@ -43,6 +43,9 @@ def test_workload_lines(wl, frames):
         assert d["fixed_cap"]["stop_mode"] == "none" and d["fixed_cap"]["frac_alg"] > 0
     if wl == "c3":
         assert d["k3"]["mframes_per_s"] > 0 and 0 < d["k3"]["share_of_step"] < 1
+        ps = d["parity_sample"]  # the cpu_baseline frames through the device: 7 points x 8 frames
+        assert ps["frames"] == 56 and ps["payload_identical"] >= 54
+        assert d["overlapped"]["value"] > 0
 
 
 @pytest.mark.gpu
