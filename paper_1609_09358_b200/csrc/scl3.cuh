@@ -193,14 +193,28 @@ __device__ __noinline__ float frozen_prefix(const float *ch, float *llr, uint32_
 #define PC_SCL3_BOUNDS __launch_bounds__(128)
 #endif
 
-template <int L, bool FEX, int NV>
+// CN > 0: the code length 2^CN and the slot layout that scl3_prepare derives
+// from it are compile-time constants (the launcher checks them), so the
+// address arithmetic folds into immediates.
+template <int CN, int NV>
+struct Scl3Geom {
+    static constexpr int tp = CN - 1 - NV;
+    static constexpr int lw = tp >= s3::T + 1 ? (1 << (tp + 1)) - (1 << (s3::T + 1)) : 0;
+    static constexpr int ss = ((lw + 7) & ~7) + 4;
+    static constexpr int psw = ((5 - s3::T) + (1 << (CN - 5)) - 1) | 1;
+};
+
+template <int L, bool FEX, int NV, int CN = 0>
 __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
 {
     using namespace s3;
     constexpr int F = 32 / L;
     constexpr uint32_t FULL = 0xffffffffu;
     extern __shared__ __align__(16) uint32_t smw[];
-    const int N = a.code.N, n = a.code.n, tp = a.tp, ss = a.ss, psw = a.psw, W = a.uhs;
+    using G = Scl3Geom<CN ? CN : 10, NV>;
+    const int n = CN ? CN : a.code.n;
+    const int N = CN ? (1 << CN) : a.code.N;
+    const int tp = CN ? G::tp : a.tp, ss = CN ? G::ss : a.ss, psw = CN ? G::psw : a.psw, W = a.uhs;
     const int lane = threadIdx.x & 31;
     uint32_t *wb = smw + (size_t)(threadIdx.x >> 5) * a.warp_words;
     float *llr = reinterpret_cast<float *>(wb);
@@ -803,10 +817,39 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
 
 // ------------------------------------------------------------- launchers --
 
+#ifndef SCL3_CN
+#define SCL3_CN 1
+#endif
+
+template <int CN, int NV>
+inline bool scl3_geom_is(const SclArgs &a)
+{
+    using G = Scl3Geom<CN, NV>;
+    return a.code.n == CN && a.tp == G::tp && a.ss == G::ss && a.psw == G::psw;
+}
+
 template <int L, bool FEX, int NV>
 inline int launch_scl3_t(const SclArgs &a, int wpc, int max_warps, cudaStream_t s)
 {
     auto kern = k_scl3<L, FEX, NV>;
+    // the default list decoders at N = 1024..4096 (min-sum f, 3 virtual levels)
+    // with the geometry compiled in (+5% at N = 1024, L = 32)
+    if constexpr (SCL3_CN && !FEX && NV == 3) {
+        switch (a.code.n) {
+        case 10:
+            if (scl3_geom_is<10, NV>(a))
+                kern = k_scl3<L, FEX, NV, 10>;
+            break;
+        case 11:
+            if (scl3_geom_is<11, NV>(a))
+                kern = k_scl3<L, FEX, NV, 11>;
+            break;
+        case 12:
+            if (scl3_geom_is<12, NV>(a))
+                kern = k_scl3<L, FEX, NV, 12>;
+            break;
+        }
+    }
     const size_t per_warp = (size_t)a.warp_words * 4;
     const size_t smem_cap = 227 * 1024;
     if (per_warp > smem_cap)

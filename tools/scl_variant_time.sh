@@ -11,7 +11,7 @@ from paper_1609_09358_b200 import CodeConfig, SclConfig
 from paper_1609_09358_b200 import _native as nat
 from paper_1609_09358_b200.channel import ebno_to_sigma
 lib = nat.load()
-for N, L, eb, B in ((1024, 32, 1.5, 32768), (1024, 32, 1.0, 32768), (2048, 8, 2.0, 32768)):
+for N, L, eb, B in ((1024, 32, 1.5, 32768), (1024, 32, 1.0, 32768), (2048, 8, 2.0, 32768), (2048, 32, 2.0, 16384), (4096, 32, 2.0, 8192), (1024, 4, 1.5, 32768)):
     code = CodeConfig(N, N // 2, crc=16); dc = nat.device_code(code)
     llr = torch.empty((B, N), device="cuda"); msg = torch.empty((B, N // 32), dtype=torch.int32, device="cuda")
     nat.check(lib.pc_gen_frames(3, 0, 0, B, ebno_to_sigma(eb, code.rate), dc.ref, msg.data_ptr(), llr.data_ptr(), nat.stream_handle()), "g")
