@@ -274,6 +274,10 @@ __device__ __forceinline__ float leaves32(float xl, uint32_t u, int lane)
     return v;
 }
 
+#ifndef SC1_CN
+#define SC1_CN 1
+#endif
+
 template <bool FEX, int G, int NV>
 __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
 {
@@ -281,7 +285,10 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
     constexpr uint32_t FULL = 0xffffffffu;
     constexpr int GL = 32 / G; // lanes per frame
     extern __shared__ __align__(16) uint32_t smw[];
-    const int N = a.code.N, n = a.code.n, NW = N >> 5;
+    // with virtual levels the launcher picked NV = n - SC1_TOP - 1: the code
+    // length is a compile-time constant then (address arithmetic in immediates)
+    const int n = (NV > 0 && SC1_CN) ? SC1_TOP + 1 + NV : a.code.n;
+    const int N = 1 << n, NW = N >> 5;
     const int lane = threadIdx.x & 31, grp = lane / GL, pl = lane % GL;
     uint32_t *colS = smw;
     uint32_t *frzS = colS + 32;
