@@ -184,6 +184,12 @@ __device__ __noinline__ float frozen_prefix(const float *ch, float *llr, uint32_
 
 } // namespace s3
 
+#ifndef SCL3_CN
+#define SCL3_CN 1
+#endif
+#ifndef SCL3_CN_ME
+#define SCL3_CN_ME 1
+#endif
 #ifndef PC_SCL3_MAXREG
 #define PC_SCL3_MAXREG 0
 #endif
@@ -225,26 +231,29 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
     float *cand = reinterpret_cast<float *>(wb + a.o_cand);
     uint32_t *wrow = wb + a.o_wrow;
     float *chs = reinterpret_cast<float *>(wb + a.o_ch);
-    const bool ch_smem = a.o_ch >= 0;
+    constexpr bool CK = CN && SCL3_CN_ME; // the compiled-in defaults (see scl3_geom_is)
+    const bool ch_smem = CK ? false : a.o_ch >= 0;
 
     const int grp = lane / L, gbase = grp * L, pl = lane - gbase;
     // the list size: L (the lanes per frame) or, for a list size that is not a
     // power of two, fewer (lanes Lc..L-1 of a frame group never hold a path)
-    const int Lc = a.list_cap > 0 && a.list_cap < L ? a.list_cap : L;
+    const int Lc = CK ? L : (a.list_cap > 0 && a.list_cap < L ? a.list_cap : L);
     const uint32_t gmask_lo = (L == 32) ? FULL : ((1u << L) - 1u);
     const int total = a.count != nullptr ? *a.count : a.B;
     float *own = llr + lane * ss;
     uint32_t *pown = ps + lane * psw;
     float *cg = cand + grp * 4 * L;
     const uint32_t *frzg = a.code.frozen_bits;
-    const uint32_t *damg = a.code.da_bits;
+    // (the compiled-in geometries also fix the default knobs: CRC on, no
+    // decision-aided positions, exact metric)
+    const uint32_t *damg = CK ? nullptr : a.code.da_bits;
     const uint32_t *colg = a.code.crc_cols;
-    const bool use_crc = a.code.crc_width > 0;
+    const bool use_crc = CK ? true : a.code.crc_width > 0;
 
     // blocks before the first non-frozen position: decoded element-parallel (below)
     // (from the code struct, not a device load: a load here costs the block walk
     // ~20% through its code generation)
-    const int nb0 = (L == 32 && a.prefix) ? a.code.first_info >> T : 0;
+    const int nb0 = (L == 32 && (CK || a.prefix)) ? a.code.first_info >> T : 0;
 
     uint32_t lp32 = 0;
     uint64_t lp64 = 0;
@@ -441,7 +450,7 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
                 if (!fz && use_crc)
                     col = SCL3_COLB ? __shfl_sync(FULL, colb, j) : __ldg(colg + i);
                 float inc0, inc1;
-                metric_incs(lam, a.metric_exact, inc0, inc1);
+                metric_incs(lam, CK ? true : (bool)a.metric_exact, inc0, inc1);
                 uint32_t u = 0u;
                 if (fz | dz) {
                     u = (dz && lam < 0.0f) ? 1u : 0u;
@@ -817,15 +826,18 @@ __global__ void PC_SCL3_BOUNDS k_scl3(const SclArgs a)
 
 // ------------------------------------------------------------- launchers --
 
-#ifndef SCL3_CN
-#define SCL3_CN 1
-#endif
 
-template <int CN, int NV>
+template <int CN, int NV, int L>
 inline bool scl3_geom_is(const SclArgs &a)
 {
     using G = Scl3Geom<CN, NV>;
-    return a.code.n == CN && a.tp == G::tp && a.ss == G::ss && a.psw == G::psw;
+    if (a.code.n != CN || a.tp != G::tp || a.ss != G::ss || a.psw != G::psw)
+        return false;
+    // the default knobs the compiled-in kernels also fix: exact metric, CRC on,
+    // no decision-aided positions, channel from global memory, a full
+    // power-of-two list, the frozen-prefix path at L = 32
+    return !SCL3_CN_ME || (a.metric_exact && a.code.crc_width > 0 && a.code.da_bits == nullptr && a.o_ch < 0 &&
+                           (a.list_cap <= 0 || a.list_cap >= L) && (L != 32 || a.prefix));
 }
 
 template <int L, bool FEX, int NV>
@@ -837,15 +849,15 @@ inline int launch_scl3_t(const SclArgs &a, int wpc, int max_warps, cudaStream_t 
     if constexpr (SCL3_CN && !FEX && NV == 3) {
         switch (a.code.n) {
         case 10:
-            if (scl3_geom_is<10, NV>(a))
+            if (scl3_geom_is<10, NV, L>(a))
                 kern = k_scl3<L, FEX, NV, 10>;
             break;
         case 11:
-            if (scl3_geom_is<11, NV>(a))
+            if (scl3_geom_is<11, NV, L>(a))
                 kern = k_scl3<L, FEX, NV, 11>;
             break;
         case 12:
-            if (scl3_geom_is<12, NV>(a))
+            if (scl3_geom_is<12, NV, L>(a))
                 kern = k_scl3<L, FEX, NV, 12>;
             break;
         }
