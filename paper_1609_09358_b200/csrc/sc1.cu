@@ -278,7 +278,9 @@ __device__ __forceinline__ float leaves32(float xl, uint32_t u, int lane)
 #define SC1_CN 1
 #endif
 
-template <bool FEX, int G, int NV>
+// DEF: the default knobs compiled in (exact metric, CRC on, no decision-aided
+// positions); the launcher picks it when the arguments match.
+template <bool FEX, int G, int NV, bool DEF = false>
 __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
 {
     using namespace sc1;
@@ -293,7 +295,8 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
     uint32_t *colS = smw;
     uint32_t *frzS = colS + 32;
     uint32_t *daS = frzS + NW;
-    const bool use_crc = a.code.crc_width > 0;
+    const bool use_crc = DEF ? true : a.code.crc_width > 0;
+    const int mex = DEF ? 1 : a.metric_exact;
     for (int i = threadIdx.x; i < N; i += blockDim.x)
         if (i < 32)
             colS[i] = 0u;
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
             // ---- the block's 32 leaves on the group's first lane, registers only
             // (K3 v3's leaf code at L = 1) ----
             uint32_t betaT = 0, bu = 0;
-            const uint32_t fzw = frzS[b], daw = daS[b];
+            const uint32_t fzw = frzS[b], daw = DEF ? 0u : daS[b];
             if (fast) {
                 // One frame per warp (latency form): the block's decisions as the fixpoint
                 // of u = rule(lambda(u)), one leaf per lane.  lambda_j depends on u_0..u_j-1
@@ -432,7 +435,7 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                 // u = 1 only if metric + inc1 < metric + inc0; a leaf decided 0 has
                 // inc0 <= inc1 and stays 0)
                 float i0v, i1v;
-                metric_incs(laml, a.metric_exact, i0v, i1v);
+                metric_incs(laml, mex, i0v, i1v);
                 const bool u1 = (u >> lane) & 1u;
                 incS[i0 + lane] = u1 ? i1v : i0v;
                 incO[i0 + lane] = u1 ? i0v : i1v;
@@ -449,14 +452,14 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                     const float4 v = *reinterpret_cast<const float4 *>(lv + t);
                     x[t] = v.x, x[t + 1] = v.y, x[t + 2] = v.z, x[t + 3] = v.w;
                 }
-                leaf_chain<FEX, true>(x, fzw, daw, use_crc ? a.code.crc_cols + i0 : colS, a.metric_exact, lam, metric,
+                leaf_chain<FEX, true>(x, fzw, daw, use_crc ? a.code.crc_cols + i0 : colS, mex, lam, metric,
                                       syn, bu, betaT);
             }
             __syncwarp();
             // the metric increments of the 32 leaves, element-parallel over the group
             for (int j = pl; j < 32; j += GL) {
                 float i0v, i1v;
-                metric_incs(lam[j], a.metric_exact, i0v, i1v);
+                metric_incs(lam[j], mex, i0v, i1v);
                 inc[2 * j] = i0v;
                 inc[2 * j + 1] = i1v;
             }
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(128) k_sc1(const SclArgs a)
                     // block from its start (metric and syndrome as they were)
                     metric = m_blk;
                     syn = s_blk;
-                    leaf_chain<FEX, false>(x, fzw, daw, use_crc ? a.code.crc_cols + i0 : colS, a.metric_exact, lam,
+                    leaf_chain<FEX, false>(x, fzw, daw, use_crc ? a.code.crc_cols + i0 : colS, mex, lam,
                                            metric, syn, bu, betaT);
                 }
                 m_blk = metric;
@@ -565,6 +568,9 @@ template <bool FEX, int G, int NV>
 static int launch_sc1_t(const SclArgs &a, cudaStream_t s, long long *capacity = nullptr)
 {
     auto kern = k_sc1<FEX, G, NV>;
+    if constexpr (!FEX && NV > 0 && SC1_CN)
+        if (a.metric_exact && a.code.crc_width > 0 && a.code.da_bits == nullptr)
+            kern = k_sc1<FEX, G, NV, true>;
     const int N = a.code.N, n = a.code.n;
     auto bytes = [&](int w) { return ((size_t)sc1::table_words<G>(N) + (size_t)w * sc1_frame_words<G>(N, n)) * 4; };
     if (bytes(1) > 227 * 1024)
