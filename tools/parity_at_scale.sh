@@ -8,4 +8,4 @@ for s in 1 2 3 4 5 6 7 8 9 10; do
   timeout 900 python tests/parity/fuzz_parity.py 440 $s > gpurun_out/${TAG}_fuzz_$s.log 2>&1
   tail -1 gpurun_out/${TAG}_fuzz_$s.log
 done
-tail -3 gpurun_out/${TAG}_scl_parity_c2.log gpurun_out/${TAG}_scl_parity_c5.log
+tail -n 3 gpurun_out/${TAG}_scl_parity_c2.log gpurun_out/${TAG}_scl_parity_c5.log
