@@ -76,6 +76,33 @@ def test_virtual_levels_do_not_change_results(nv):
         assert torch.equal(mt, base.metric)
 
 
+@pytest.mark.parametrize("N,L", [(1024, 4), (2048, 8), (2048, 32), (4096, 32)])
+def test_compiled_in_kernels_match_runtime_kernels(N, L):
+    """The default configuration runs K3 kernels with the code geometry and
+    the default knobs compiled in (k_scl3<L, false, 3, n>); two virtual levels
+    select the runtime-parameter kernel, which must give the same bits
+    (virtual levels never change results)."""
+    from paper_1609_09358_b200 import _native as nat
+    import ctypes
+    import torch
+
+    code = CodeConfig(N, N // 2, crc=16)
+    sigma = ebno_to_sigma(1.5, code.rate)
+    B = 64
+    llrs = np.array([make_frame(code, sigma, frame_rng(62, N, f))[1] for f in range(B)])
+    x = torch.from_numpy(llrs.astype(np.float32)).cuda()
+    base = scl_decode_batch(x, code, SclConfig(L))
+    cfg = SclConfig(L).native(virtual_levels=2)
+    dc = nat.device_code(code)
+    u = torch.zeros_like(base.u_hat)
+    mt = torch.zeros_like(base.metric)
+    nat.check(nat.load().pc_scl_decode(x.data_ptr(), B, None, None, dc.ref, ctypes.byref(cfg), u.data_ptr(), None,
+                                       mt.data_ptr(), None, None, None, dc.scl_workspace(cfg).data_ptr(),
+                                       nat.stream_handle()), "scl")
+    assert torch.equal(u, base.u_hat)
+    assert torch.equal(mt, base.metric)
+
+
 @pytest.mark.parametrize("N,k,L,eb,count", [(1024, 512, 32, 1.5, 400), (1024, 512, 4, 1.0, 400),
                                             (2048, 1024, 16, 2.0, 100), (64, 32, 2, 1.0, 400),
                                             (2048, 1024, 32, 1.5, 300), (2048, 1024, 1, 2.0, 1000),
