@@ -91,6 +91,9 @@ __device__ __forceinline__ void b_c(const float (&v)[8], float (&o)[8], float *x
 
 } // namespace b3
 
+#ifndef PC_BP3_MINB12
+#define PC_BP3_MINB12 1 // N = 4096: the one CTA per SM may use up to 128 registers (119; +0.6%)
+#endif
 #ifndef PC_BP3_MINB10
 #define PC_BP3_MINB10 5 // N = 1024: 5 CTAs per SM (96 registers; +0.7% over the compiler's own choice)
 #endif
@@ -105,7 +108,8 @@ __host__ __device__ constexpr int bp3_smem_floats(int logn)
 }
 
 template <int LOGN, int GMODE, bool RE, bool PERS>
-__global__ void __launch_bounds__((1 << LOGN) / 8, (LOGN == 10 && GMODE == 0) ? PC_BP3_MINB10 : 0) k_bp3(const BpArgs a)
+__global__ void __launch_bounds__((1 << LOGN) / 8, (LOGN == 10 && GMODE == 0) ? PC_BP3_MINB10
+                                                   : ((LOGN == 12 && GMODE == 0) ? PC_BP3_MINB12 : 0)) k_bp3(const BpArgs a)
 {
     using namespace b3;
     constexpr int N = 1 << LOGN;

@@ -91,14 +91,19 @@ __device__ __forceinline__ void b_c(const float (&v)[8], float (&o)[8], float *x
 
 } // namespace b3h
 
-constexpr int BP3H_WARPS = 4; // warps per CTA (8 frames)
+#ifndef PC_BP3H_WARPS
+#define PC_BP3H_WARPS 4
+#endif
+constexpr int BP3H_WARPS = PC_BP3H_WARPS; // warps per CTA (2 frames each)
 
 #ifndef PC_BP3H_MINB
 #define PC_BP3H_MINB 4 // 128 registers: 4 CTAs per SM (measured best; 5 and 6 were slower)
 #endif
 
+// (the default form gets the compiler's own choice, 128 registers: 1.8% faster than
+// its choice under the 4-CTA bound; the others are held to 128 by the bound)
 template <int GMODE, bool PERS, bool RE>
-__global__ void __launch_bounds__(32 * BP3H_WARPS, PC_BP3H_MINB) k_bp3h(const BpArgs a)
+__global__ void __launch_bounds__(32 * BP3H_WARPS, (GMODE == 0 && !RE) ? 1 : PC_BP3H_MINB) k_bp3h(const BpArgs a)
 {
     using namespace b3h;
     constexpr int N = 128, Q = 8, NW = N / 32;
