@@ -15,7 +15,11 @@ frame latency, gamma and FER are in "sweep".
     python bench.py --workload c5     # BASELINE configs[4]: SCL N=2048 list-size sweep L=1..32
 
 The default workload (c3) is the headline; the others print their own JSON
-line (same contract keys) for the other BASELINE configurations.
+line (same contract keys) for the other BASELINE configurations.  c3 times
+the points one after another (value, roofline and shares come from that
+region) and then the same steps with the cross-point overlap ("overlapped");
+"e2e" runs the public host-buffer call; "parity_sample" decodes the
+cpu_baseline frames on the device beside the oracle's results.
 
 Multi-GPU: frames shard by index (weak scaling, no collective on the data
 path); timing is the max over ranks of the barrier-bracketed device time.
