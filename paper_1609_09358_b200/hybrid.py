@@ -440,6 +440,8 @@ class HybridDecoder:
             with torch.cuda.graph(g, stream=side):
                 self.run(llr, B)  # enqueued on the BP / SCL streams, which join the capture
             cur.wait_stream(side)
+            if len(graphs) >= 8:  # a bounded cache: drop the oldest capture
+                graphs.pop(next(iter(graphs)))
             graphs[key] = g
             return self
         g.replay()
